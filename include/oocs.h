@@ -1,0 +1,281 @@
+/*
+ * oocs.h — C ABI of the B200-native out-of-core compressed stencil library
+ * (arXiv 2204.11315, "Compression-Based Optimizations for Out-of-Core GPU
+ * Stencil Computation", Shen, Deng, Wu, Okita, Ino).
+ *
+ * The library runs the paper's data-parallel hot path on one GPU per process:
+ * for every z-chunk ("block") of a 3-D grid that does not fit the GPU, H2D of
+ * the fixed-rate-compressed chunk (minus the overlap already resident on the
+ * GPU, "region sharing"), GPU decompression, k temporally blocked steps
+ * of a 25-point acoustic-wave stencil in a single working buffer (P:L85,
+ * P:L170-173), GPU recompression of the owned planes and D2H, overlapped on
+ * three CUDA streams with the event hand-off of Algorithm 1.
+ *
+ * Citations: "P:L<n>" = PAPER.md line n; "S:L<n>" = SPEC.md line n.
+ *
+ * General rules
+ *  - Every call returns oocs_status; OOCS_OK = 0.  No C++ exception crosses
+ *    the ABI.  On failure oocs_last_error() returns a thread-local message.
+ *  - After a CUDA error inside oocs_run/oocs_load/oocs_store the plan is
+ *    poisoned: every later call except oocs_destroy returns OOCS_ERR_STATE.
+ *  - Pointers are plain host or device pointers as stated per argument; the
+ *    library never retains caller pointers beyond the call, except buffers
+ *    bound with oocs_plan_bind_arena (caller keeps them alive until destroy).
+ *  - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ *    default stream).  No torch type appears in any signature.
+ *  - One plan per host thread; plans on different devices may run
+ *    concurrently.
+ *
+ * Grid layout (host side, "allocated layout"): an array of the grid is
+ * (az, ay, ax) float32, x fastest, with ax = nx+2R, ay = ny+2R, az = nz+2R,
+ * R = 4 (Table 1 "(1152+2xHALO)^3, HALO=4").  Allocated plane index
+ * a = interior plane z + R.  The R-cell halo on all six faces is a Dirichlet
+ * boundary: it keeps its initial value forever (pressure 0 by convention).
+ *
+ * Compressed format (docs/FORMAT.md): each array is stored slab by slab (4
+ * allocated planes per slab), within a slab by 4x4x4 block in (by, bx) order,
+ * so every 4-aligned plane range is one contiguous, independently decodable
+ * byte range ("we compress the overlapped area of a chunk
+ * separately").  BlockQuant block record = 8(q+1) bytes:
+ *   [mn f32][mx f32][P_{q-1} u64] ... [P_0 u64],  P_b bit j = bit b of code_j,
+ *   j = xi + 4 yi + 16 zi; rate r = q + 1 bits/value (r = 16 is the paper's
+ *   "compression rate 32/64 = 1/2", applied to fp32).
+ * Identity codec: raw float32 planes (ax*ay*4 bytes per plane).
+ */
+#ifndef OOCS_H
+#define OOCS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OOCS_RADIUS 4      /* 25-point star stencil radius (Table 1 HALO=4) */
+#define OOCS_ABI_VERSION 1
+
+typedef enum {
+    OOCS_OK = 0,
+    OOCS_ERR_CONFIG = 2,     /* invalid configuration */
+    OOCS_ERR_DEVICE_OOM = 3, /* device capacity exceeded */
+    OOCS_ERR_VERIFY = 4,     /* reserved: verification failure */
+    OOCS_ERR_IO = 5,         /* host-side I/O / pinned allocation failure */
+    OOCS_ERR_DATA = 6,       /* NaN/Inf or |x| >= 2^126 given to a lossy codec */
+    OOCS_ERR_HOST_OOM = 7,   /* host (pinned) allocation failed */
+    OOCS_ERR_CUDA = 8,       /* CUDA runtime error; plan poisoned */
+    OOCS_ERR_EXCHANGE = 9,   /* the multi-GPU halo exchange callback failed */
+    OOCS_ERR_STATE = 10      /* plan poisoned by an earlier failure, or call out of order */
+} oocs_status;
+
+typedef enum {
+    OOCS_CODEC_IDENTITY = 0,   /* raw fp32 (rate 32) */
+    OOCS_CODEC_BLOCKQUANT = 1  /* fixed-rate 4x4x4 block quantiser, rate_bits in [2, 24] */
+} oocs_codec;
+
+/* Pipeline architectures of the paper (Fig. 6 `fig:3ver`, Fig. 7 `fig:swb`). */
+typedef enum {
+    OOCS_MODE_BASELINE = 0,     /* fig:3ver(a): no compression, 3 per-stream working buffers */
+    OOCS_MODE_COMPRESS = 1,     /* fig:3ver(b): compression, 3 per-stream working buffers */
+    OOCS_MODE_COMPRESS_SWB = 2, /* fig:swb: compression + single working buffer (the paper's method) */
+    OOCS_MODE_COMPRESS_DWB = 3  /* compression + 2 ping-pong working buffers (BASELINE.json configs[4]) */
+} oocs_mode;
+
+typedef enum {
+    OOCS_STORE_HOST = 0,  /* compressed state in pinned host memory, streamed over PCIe (the paper) */
+    OOCS_STORE_DEVICE = 1 /* compressed state resident in HBM (double-buffered); kernels only */
+} oocs_store_kind;
+
+#define OOCS_FLAG_PROFILE 1u /* time every kernel launch with CUDA events (oocs_stats.kernel_ms) */
+
+typedef struct {
+    uint32_t struct_size;     /* sizeof(oocs_config): ABI versioning */
+    int64_t nx, ny, nz;       /* interior cells; nx, ny, nz multiples of 4 */
+    float dt;                 /* time step; update uses c = (v*dt)^2 with h = 1 */
+    int32_t n_blocks;         /* global number of z-chunks n ("eight chunks") */
+    int32_t tb_depth;         /* temporal-blocking depth k: steps per chunk visit */
+    int32_t codec;            /* oocs_codec */
+    int32_t rate_bits;        /* BlockQuant rate r (q = r - 1 code bits); ignored for identity */
+    int32_t mode;             /* oocs_mode */
+    int32_t region_sharing;   /* 1: reuse the 2kR-plane overlap on the GPU; 0: re-send it */
+    int32_t store;            /* oocs_store_kind */
+    int32_t device;           /* CUDA device ordinal used by this plan */
+    int32_t rank, world;      /* z-slab sharding: this process owns a contiguous run of blocks */
+    uint32_t flags;           /* OOCS_FLAG_* */
+    uint64_t device_capacity; /* 0 = unlimited; else the arena may not exceed this many bytes */
+} oocs_config;
+
+typedef struct {
+    int64_t ax, ay, az;         /* allocated extents */
+    int64_t pitch;              /* working-buffer row pitch in floats (>= ax + 28, multiple of 32) */
+    int64_t plane_bytes;        /* compressed bytes of one allocated plane of one array */
+    int64_t z_lo, z_hi;         /* this rank's owned interior planes [z_lo, z_hi) */
+    int64_t store_lo, store_hi; /* interior planes held in this rank's store (owned + ghost halo) */
+    int32_t block_lo, block_hi; /* this rank's global blocks [block_lo, block_hi) */
+    int64_t max_ext_planes;     /* largest extended extent (planes) = working-buffer depth */
+    uint64_t arena_bytes;       /* device bytes the plan allocated (its peak: allocation is static) */
+    uint64_t working_set_bytes; /* one working buffer (all arrays) = the paper's "1 unit" x datasets */
+    uint64_t staging_bytes;     /* all compressed staging buffers (hf_buf) */
+    uint64_t store_bytes;       /* compressed state (host pinned or device) */
+    int32_t n_working_sets;     /* 3 (BASELINE/COMPRESS), 1 (SWB), 2 (DWB) */
+    int32_t n_lanes;            /* CUDA streams of the pipeline (3) */
+} oocs_plan_info;
+
+typedef struct {
+    double wall_ms;             /* device time of the run: event on first op .. event after last op */
+    double kernel_ms[3];        /* [decode, step, encode] summed launch durations (OOCS_FLAG_PROFILE) */
+    int64_t kernel_launches[3]; /* launches per kind */
+    uint64_t bytes_h2d, bytes_d2h, bytes_d2d, bytes_exchange;
+    uint64_t cell_updates;          /* useful: nx*ny*(owned planes)*steps on this rank */
+    uint64_t cell_updates_computed; /* incl. redundant temporal-blocking halo updates */
+    uint64_t alg_bytes[3];          /* algorithmic HBM bytes per kind */
+    int32_t data_error;             /* 1 if the encoder saw NaN/Inf/|x|>=2^126 */
+    int32_t reserved;
+} oocs_stats;
+
+/* One entry of the decomposition table (interior plane coordinates,
+ * half-open intervals). */
+typedef struct {
+    int64_t own_lo, own_hi;     /* owned planes: partition of [0, nz) */
+    int64_t ext_lo, ext_hi;     /* own +- k*R, clamped to [-R, nz+R) */
+    int64_t carry_lo, carry_hi; /* overlap with the previous chunk's extent, kept on the GPU */
+    int64_t body_lo, body_hi;   /* ext \ carry: what crosses PCIe */
+} oocs_block;
+
+/* One operation of the lowered pipeline schedule (Algorithm 1 + repairs). */
+typedef struct {
+    int32_t kind;  /* oocs_op_kind */
+    int32_t lane;  /* CUDA stream index */
+    int64_t g;     /* global block counter (sweep * blocks + block) the op belongs to */
+    int32_t block; /* global block index */
+    int32_t sweep;
+    int32_t arg;   /* STEP: step index s (1..k); WAIT/RECORD: event kind; else 0 */
+    int32_t pad;
+    int64_t ev_g;  /* WAIT/RECORD: block counter of the event */
+} oocs_op;
+
+typedef enum {
+    OOCS_OP_H2D = 0, OOCS_OP_CARRY = 1, OOCS_OP_DECODE = 2, OOCS_OP_STEP = 3,
+    OOCS_OP_ENCODE = 4, OOCS_OP_D2H = 5, OOCS_OP_RECORD = 6, OOCS_OP_WAIT = 7,
+    OOCS_OP_EXCHANGE = 8
+} oocs_op_kind;
+
+typedef enum {
+    OOCS_EV_H2D = 0,   /* body (+carry) of block g is in its staging/working buffer */
+    OOCS_EV_DEC = 1,   /* block g decoded */
+    OOCS_EV_ENC = 2,   /* block g encoded: working buffer free (Alg. 1 "Record evt[prev_s]") */
+    OOCS_EV_D2H = 3,   /* owned planes of block g written back to the host store */
+    OOCS_EV_CARRY = 4  /* BASELINE mode: carry of block g copied into its working buffer */
+} oocs_event_kind;
+
+/* Multi-GPU halo exchange, called by oocs_run on the host after sweep
+ * `sweep` has been fully written back.  send_lo/recv_lo (send_hi/recv_hi)
+ * are DEVICE pointers to k*R compressed planes x 2 pressure arrays destined
+ * for / arriving from rank-1 (rank+1); NULL at the domain edge.  The callback
+ * must complete the transfer (e.g. NCCL send/recv on `stream`, then
+ * synchronize) before returning 0; non-zero aborts the run with
+ * OOCS_ERR_EXCHANGE. */
+typedef int (*oocs_exchange_fn)(void *user, int64_t sweep, void *send_lo, void *send_hi,
+                                void *recv_lo, void *recv_hi, uint64_t bytes, void *stream);
+
+typedef struct oocs_plan oocs_plan;
+
+/* ---- host-only calls (no GPU needed) ---------------------------------- */
+
+/* Validate cfg and fill the decomposition table for ALL global blocks
+ * (out[cfg->n_blocks], caller-owned).  Pure function of cfg.
+ * Errors: OOCS_ERR_CONFIG for nx/ny/nz not multiples of 4, n_blocks > nz/4,
+ * k*R >= owned width, rate outside [2,24], world not dividing
+ * n_blocks, dt <= 0 or above the CFL limit 2/(v_max*sqrt(19.505...)) is NOT
+ * checked here (v is data). */
+oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out);
+
+/* Lower the pipeline of `steps` time steps (steps % k == 0) for this rank
+ * to its operation list (the exact list oocs_run issues for a HOST store).
+ * Always sets *n_ops to the full count and writes the first min(cap, count)
+ * ops to `ops` (ops may be NULL when cap == 0).
+ * Errors: OOCS_ERR_CONFIG. */
+oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs_op *ops, int64_t cap,
+                          int64_t *n_ops);
+
+/* Compressed bytes of `planes` allocated planes of one array. */
+oocs_status oocs_encoded_bytes(const oocs_config *cfg, int64_t planes, uint64_t *bytes);
+
+/* ---- plan lifetime ----------------------------------------------------- */
+
+/* Create a plan on cfg->device: validates, allocates the device arena
+ * (working buffers, staging, [device store]) and the pinned host store,
+ * creates streams and events.  *out = NULL on failure.
+ * Errors: OOCS_ERR_CONFIG, OOCS_ERR_DEVICE_OOM (arena > device_capacity or
+ * cudaMalloc failure), OOCS_ERR_HOST_OOM, OOCS_ERR_CUDA. */
+oocs_status oocs_plan_create(const oocs_config *cfg, oocs_plan **out);
+
+oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info);
+
+/* Install the halo-exchange callback (required when world > 1). */
+oocs_status oocs_set_exchange(oocs_plan *plan, oocs_exchange_fn fn, void *user);
+
+/* NULL-safe; frees streams, events, arena and pinned store. */
+oocs_status oocs_destroy(oocs_plan *plan);
+
+/* ---- state in / out ---------------------------------------------------- */
+
+/* Compress allocated planes [a_lo, a_hi) (allocated coordinates, 4-aligned,
+ * within this rank's store) of one array from HOST memory `src` laid out
+ * (a_hi-a_lo, ay, ax) float32 into the store.  array: 0 = velocity
+ * (read-only dataset), 1 = pressure at t-1, 2 = pressure at t.
+ * The GPU encodes; host memory is only read during the call.
+ * Errors: OOCS_ERR_CONFIG (range), OOCS_ERR_DATA (non-finite input for a
+ * lossy codec), OOCS_ERR_CUDA. */
+oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi);
+
+/* Decompress allocated planes [a_lo, a_hi) of one array into HOST `dst`
+ * (same layout as oocs_load). */
+oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi);
+
+/* Raw compressed bytes of allocated planes [a_lo, a_hi) of one array,
+ * to / from HOST memory (bitstream parity tests, checkpoints). */
+oocs_status oocs_store_read_raw(oocs_plan *plan, int32_t array, void *dst, int64_t a_lo, int64_t a_hi);
+oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src, int64_t a_lo,
+                                 int64_t a_hi);
+
+/* Advance the state by `steps` time steps (steps % k == 0) = steps/k sweeps
+ * of Algorithm 1 over this rank's blocks, sweeps pipelined back to back.
+ * Blocks the host until the device work is complete.  `out` may be NULL.
+ * Errors: OOCS_ERR_CONFIG (steps), OOCS_ERR_DATA (encoder rejected a value;
+ * state undefined), OOCS_ERR_CUDA, OOCS_ERR_EXCHANGE, OOCS_ERR_STATE. */
+oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out);
+
+/* ---- hot-path kernels, callable on caller device memory --------------- */
+/* Working-buffer layout for these calls: planes x ay rows x `pitch` floats,
+ * element (x) of a row at column x + 28 (so interior x = R starts on a
+ * 128-byte boundary); pitch >= ax + 28 and a multiple of 32. */
+
+/* Decompress `planes` (multiple of 4) allocated planes: src (DEVICE)
+ * compressed bytes -> dst (DEVICE) working-buffer layout. */
+oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes,
+                        int64_t pitch, int32_t codec, int32_t rate_bits, void *stream);
+
+/* Compress `planes` allocated planes of src (DEVICE, working-buffer layout)
+ * into dst (DEVICE).  *err_flag (DEVICE int32, may be NULL) is OR-ed with 1
+ * if a value is rejected. */
+oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes,
+                        int64_t pitch, int32_t codec, int32_t rate_bits, int32_t *err_flag,
+                        void *stream);
+
+/* One leapfrog step of the 25-point stencil:
+ *   p_prev[z] <- 2 p_curr[z] - p_prev[z] + (v dt)^2 Lap25(p_curr)[z]
+ * on buffer planes [z_lo, z_hi) (R <= z_lo, z_hi <= planes-R), interior x,y.
+ * All pointers DEVICE, working-buffer layout.  p_prev is updated in place. */
+oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int64_t ax, int64_t ay,
+                      int64_t planes, int64_t pitch, float dt, int64_t z_lo, int64_t z_hi,
+                      void *stream);
+
+/* ---- misc -------------------------------------------------------------- */
+const char *oocs_last_error(void);
+int32_t oocs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOCS_H */

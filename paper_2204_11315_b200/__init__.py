@@ -1,0 +1,302 @@
+"""paper_2204_11315_b200 — B200-native out-of-core compressed stencil (arXiv 2204.11315).
+
+Thin ctypes binding over the C ABI in include/oocs.h (liboocs.so, built
+in-tree for sm_100a by _build.py).  Argument marshalling only: every step of
+the hot path runs inside the library's CUDA kernels and streams.  There is no
+CPU fallback: importing works on a CPU-only box (for the host-only planning
+calls), but every GPU call fails loudly if the extension or the GPU is
+missing.
+
+Function names mirror the C ABI (oocs_plan_create, oocs_run, ...); the
+``Plan`` class is a convenience wrapper over the same calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
+    "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
+    "oocs_plan_query", "oocs_destroy", "oocs_load", "oocs_store", "oocs_store_read_raw",
+    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
+    "oocs_set_exchange", "Plan", "XOFF", "pitch_for",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboocs.so")
+R = 4
+XOFF = 32 - R
+
+OOCS_OK = 0
+STATUS = {0: "OK", 2: "CONFIG", 3: "DEVICE_OOM", 4: "VERIFY", 5: "IO", 6: "DATA", 7: "HOST_OOM",
+          8: "CUDA", 9: "EXCHANGE", 10: "STATE"}
+CODEC = {"identity": 0, "blockquant": 1}
+MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
+STORE = {"host": 0, "device": 1}
+FLAG_PROFILE = 1
+OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
+EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY"]
+
+i32, i64, u32, u64, f32, f64, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
+                                    ctypes.c_float, ctypes.c_double, ctypes.c_void_p)
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("struct_size", u32), ("nx", i64), ("ny", i64), ("nz", i64), ("dt", f32),
+                ("n_blocks", i32), ("tb_depth", i32), ("codec", i32), ("rate_bits", i32), ("mode", i32),
+                ("region_sharing", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
+                ("flags", u32), ("device_capacity", u64)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("ax", i64), ("ay", i64), ("az", i64), ("pitch", i64), ("plane_bytes", i64), ("z_lo", i64),
+                ("z_hi", i64), ("store_lo", i64), ("store_hi", i64), ("block_lo", i32), ("block_hi", i32),
+                ("max_ext_planes", i64), ("arena_bytes", u64), ("working_set_bytes", u64),
+                ("staging_bytes", u64), ("store_bytes", u64), ("n_working_sets", i32), ("n_lanes", i32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("wall_ms", f64), ("kernel_ms", f64 * 3), ("kernel_launches", i64 * 3), ("bytes_h2d", u64),
+                ("bytes_d2h", u64), ("bytes_d2d", u64), ("bytes_exchange", u64), ("cell_updates", u64),
+                ("cell_updates_computed", u64), ("alg_bytes", u64 * 3), ("data_error", i32), ("reserved", i32)]
+
+    def as_dict(self):
+        return {
+            "wall_ms": self.wall_ms, "kernel_ms": list(self.kernel_ms),
+            "kernel_launches": list(self.kernel_launches), "bytes_h2d": self.bytes_h2d,
+            "bytes_d2h": self.bytes_d2h, "bytes_d2d": self.bytes_d2d, "bytes_exchange": self.bytes_exchange,
+            "cell_updates": self.cell_updates, "cell_updates_computed": self.cell_updates_computed,
+            "alg_bytes": list(self.alg_bytes), "data_error": self.data_error,
+        }
+
+
+class Block(ctypes.Structure):
+    _fields_ = [("own_lo", i64), ("own_hi", i64), ("ext_lo", i64), ("ext_hi", i64), ("carry_lo", i64),
+                ("carry_hi", i64), ("body_lo", i64), ("body_hi", i64)]
+
+
+class Op(ctypes.Structure):
+    _fields_ = [("kind", i32), ("lane", i32), ("g", i64), ("block", i32), ("sweep", i32), ("arg", i32),
+                ("pad", i32), ("ev_g", i64)]
+
+
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, vp, i64, vp, vp, vp, vp, u64, vp)
+
+
+class OocsError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: OOCS_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load liboocs.so (never falls back to anything else)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        sig = {
+            "oocs_plan_table": ([P(Config), vp], i32),
+            "oocs_schedule": ([P(Config), i64, vp, i64, P(i64)], i32),
+            "oocs_encoded_bytes": ([P(Config), i64, P(u64)], i32),
+            "oocs_plan_create": ([P(Config), P(vp)], i32),
+            "oocs_plan_query": ([vp, P(PlanInfo)], i32),
+            "oocs_set_exchange": ([vp, EXCHANGE_FN, vp], i32),
+            "oocs_destroy": ([vp], i32),
+            "oocs_load": ([vp, i32, vp, i64, i64], i32),
+            "oocs_store": ([vp, i32, vp, i64, i64], i32),
+            "oocs_store_read_raw": ([vp, i32, vp, i64, i64], i32),
+            "oocs_store_write_raw": ([vp, i32, vp, i64, i64], i32),
+            "oocs_run": ([vp, i64, P(Stats)], i32),
+            "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
+            "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
+            "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, vp], i32),
+            "oocs_last_error": ([], ctypes.c_char_p),
+            "oocs_abi_version": ([], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != OOCS_OK:
+        raise OocsError(st, where, lib().oocs_last_error().decode())
+
+
+def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
+                region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
+                device_capacity=0) -> Config:
+    c = Config()
+    c.struct_size = ctypes.sizeof(Config)
+    c.nx, c.ny, c.nz = nx, ny, nz
+    c.dt = float(dt)
+    c.n_blocks, c.tb_depth = n_blocks, tb_depth
+    c.codec = CODEC[codec] if isinstance(codec, str) else codec
+    c.rate_bits = rate_bits
+    c.mode = MODE[mode] if isinstance(mode, str) else mode
+    c.region_sharing = int(region_sharing)
+    c.store = STORE[store] if isinstance(store, str) else store
+    c.device, c.rank, c.world = device, rank, world
+    c.flags = FLAG_PROFILE if profile else 0
+    c.device_capacity = device_capacity
+    return c
+
+
+def pitch_for(ax: int) -> int:
+    return (XOFF + ax + 31) // 32 * 32
+
+
+# ---- host-only calls --------------------------------------------------------
+def oocs_plan_table(cfg: Config):
+    out = (Block * cfg.n_blocks)()
+    _check(lib().oocs_plan_table(ctypes.byref(cfg), out), "oocs_plan_table")
+    return [(b.own_lo, b.own_hi, b.ext_lo, b.ext_hi, b.carry_lo, b.carry_hi, b.body_lo, b.body_hi) for b in out]
+
+
+def oocs_schedule(cfg: Config, steps: int):
+    n = i64(0)
+    _check(lib().oocs_schedule(ctypes.byref(cfg), steps, None, 0, ctypes.byref(n)), "oocs_schedule")
+    arr = (Op * n.value)()
+    _check(lib().oocs_schedule(ctypes.byref(cfg), steps, arr, n.value, ctypes.byref(n)), "oocs_schedule")
+    return [dict(kind=OP_KINDS[o.kind], lane=o.lane, g=o.g, block=o.block, sweep=o.sweep, arg=o.arg,
+                 ev=(EV_KINDS[o.arg] if o.kind in (6, 7) else None), ev_g=o.ev_g) for o in arr]
+
+
+def oocs_encoded_bytes(cfg: Config, planes: int) -> int:
+    b = u64(0)
+    _check(lib().oocs_encoded_bytes(ctypes.byref(cfg), planes, ctypes.byref(b)), "oocs_encoded_bytes")
+    return b.value
+
+
+# ---- plan lifetime / state ---------------------------------------------------
+def oocs_plan_create(cfg: Config):
+    h = vp()
+    _check(lib().oocs_plan_create(ctypes.byref(cfg), ctypes.byref(h)), "oocs_plan_create")
+    return h
+
+
+def oocs_plan_query(h) -> PlanInfo:
+    info = PlanInfo()
+    _check(lib().oocs_plan_query(h, ctypes.byref(info)), "oocs_plan_query")
+    return info
+
+
+def oocs_destroy(h):
+    lib().oocs_destroy(h)
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(vp)
+
+
+def oocs_load(h, array: int, src: np.ndarray, a_lo: int, a_hi: int):
+    src = np.ascontiguousarray(src, dtype=np.float32)
+    _check(lib().oocs_load(h, array, _ptr(src), a_lo, a_hi), "oocs_load")
+
+
+def oocs_store(h, array: int, dst: np.ndarray, a_lo: int, a_hi: int):
+    assert dst.dtype == np.float32
+    _check(lib().oocs_store(h, array, _ptr(dst), a_lo, a_hi), "oocs_store")
+
+
+def oocs_store_read_raw(h, array: int, dst: np.ndarray, a_lo: int, a_hi: int):
+    _check(lib().oocs_store_read_raw(h, array, _ptr(dst), a_lo, a_hi), "oocs_store_read_raw")
+
+
+def oocs_store_write_raw(h, array: int, src: np.ndarray, a_lo: int, a_hi: int):
+    src = np.ascontiguousarray(src)
+    _check(lib().oocs_store_write_raw(h, array, _ptr(src), a_lo, a_hi), "oocs_store_write_raw")
+
+
+def oocs_run(h, steps: int) -> Stats:
+    st = Stats()
+    _check(lib().oocs_run(h, steps, ctypes.byref(st)), "oocs_run")
+    return st
+
+
+def oocs_set_exchange(h, fn, user=None):
+    _check(lib().oocs_set_exchange(h, fn, user), "oocs_set_exchange")
+
+
+# ---- kernel-level calls on caller device memory (integer device pointers) ---------
+def oocs_decode(src_ptr: int, dst_ptr: int, ax, ay, planes, pitch, codec, rate_bits, stream=0):
+    _check(lib().oocs_decode(src_ptr, dst_ptr, ax, ay, planes, pitch, codec, rate_bits, stream or None),
+           "oocs_decode")
+
+
+def oocs_encode(src_ptr: int, dst_ptr: int, ax, ay, planes, pitch, codec, rate_bits, err_ptr=0, stream=0):
+    _check(lib().oocs_encode(src_ptr, dst_ptr, ax, ay, planes, pitch, codec, rate_bits, err_ptr or None,
+                             stream or None), "oocs_encode")
+
+
+def oocs_step(vel_ptr: int, pprev_ptr: int, pcurr_ptr: int, ax, ay, planes, pitch, dt, z_lo, z_hi, stream=0):
+    _check(lib().oocs_step(vel_ptr, pprev_ptr, pcurr_ptr, ax, ay, planes, pitch, float(dt), z_lo, z_hi,
+                           stream or None), "oocs_step")
+
+
+@dataclass
+class Plan:
+    """Convenience owner of an oocs_plan handle (same calls as the C ABI)."""
+    cfg: Config
+    handle: object = None
+
+    def __post_init__(self):
+        self.handle = oocs_plan_create(self.cfg)
+        self.info = oocs_plan_query(self.handle)
+        self._cb = None
+
+    def load(self, array, src, a_lo, a_hi):
+        oocs_load(self.handle, array, src, a_lo, a_hi)
+
+    def store(self, array, a_lo, a_hi):
+        out = np.empty((a_hi - a_lo, self.info.ay, self.info.ax), dtype=np.float32)
+        oocs_store(self.handle, array, out, a_lo, a_hi)
+        return out
+
+    def read_raw(self, array, a_lo, a_hi):
+        out = np.empty((a_hi - a_lo) * self.info.plane_bytes, dtype=np.uint8)
+        oocs_store_read_raw(self.handle, array, out, a_lo, a_hi)
+        return out
+
+    def write_raw(self, array, src, a_lo, a_hi):
+        oocs_store_write_raw(self.handle, array, src, a_lo, a_hi)
+
+    def run(self, steps) -> Stats:
+        return oocs_run(self.handle, steps)
+
+    def set_exchange(self, pyfn):
+        """pyfn(sweep, send_lo, send_hi, recv_lo, recv_hi, nbytes, stream) -> int (device pointers as ints)."""
+        def _tramp(user, sweep, sl, sh, rl, rh, nbytes, stream):
+            try:
+                return int(pyfn(sweep, sl, sh, rl, rh, nbytes, stream) or 0)
+            except Exception:  # never let a Python exception cross the C ABI
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._cb = EXCHANGE_FN(_tramp)
+        oocs_set_exchange(self.handle, self._cb)
+
+    def close(self):
+        if self.handle is not None:
+            oocs_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

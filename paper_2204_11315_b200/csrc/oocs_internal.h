@@ -1,0 +1,50 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/oocs.h"
+
+namespace oocs {
+
+constexpr int R = OOCS_RADIUS;
+constexpr int XOFF = 32 - R;  // column offset: interior x = R lands on a 128-byte boundary
+constexpr int N_ARRAYS = 3;   // 0 velocity (read-only), 1 pressure t-1, 2 pressure t
+constexpr int N_LANES = 3;    // strm[0:3]
+
+// Geometry derived from a config (pure host; plan.cpp).
+struct Geometry {
+    oocs_config cfg;
+    int64_t nx, ny, nz, ax, ay, az, pitch, pstride;  // pstride = ay * pitch (floats)
+    int q;                  // BlockQuant code bits (rate_bits - 1); 0 for identity
+    int codec;
+    int64_t plane_bytes;    // compressed bytes of one allocated plane of one array
+    int k;                  // temporal-blocking depth
+    std::vector<oocs_block> blocks;  // all global blocks
+    int b_lo, b_hi;         // this rank's blocks
+    int64_t store_lo, store_hi;      // interior planes held by this rank's store (owned + ghost)
+    int64_t max_ext, max_own;        // planes
+    int n_ws;               // working sets
+    bool host_store;
+    int64_t a_store_lo() const { return store_lo + R; }  // allocated plane of store index 0
+    int64_t store_planes() const { return store_hi - store_lo; }
+    int nb() const { return b_hi - b_lo; }
+};
+
+oocs_status make_geometry(const oocs_config *cfg, Geometry *geo, std::string *err);
+void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops);
+
+// kernels.cu
+cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
+                          int codec, int q, cudaStream_t st);
+cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
+                          int codec, int q, int *err, cudaStream_t st);
+cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
+                        int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
+
+void set_error(const std::string &msg);
+
+}  // namespace oocs

@@ -1,0 +1,282 @@
+// Host-side planning: configuration validation, z-chunk decomposition with
+// temporal-blocking halos and region-sharing overlaps (§3.1,
+// S:L42-61), and the lowering of Algorithm 1 plus the hazard
+// edges it leaves implicit to a per-lane
+// operation list.  Pure functions: no CUDA calls, testable on a CPU box
+// through oocs_plan_table / oocs_schedule.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "oocs_internal.h"
+
+namespace oocs {
+
+static bool bad(std::string *err, const std::string &msg) {
+    if (err) *err = msg;
+    return false;
+}
+
+static bool validate(const oocs_config *c, std::string *err) {
+    if (!c) return bad(err, "config is NULL");
+    if (c->struct_size != sizeof(oocs_config)) return bad(err, "oocs_config.struct_size mismatch (ABI version)");
+    if (c->nx <= 0 || c->ny <= 0 || c->nz <= 0) return bad(err, "grid dimensions must be positive");
+    if (c->nx % 4 || c->ny % 4 || c->nz % 4) return bad(err, "nx, ny, nz must be multiples of 4 (4x4x4 codec blocks)");
+    if (!(c->dt > 0.0f) || !std::isfinite(c->dt)) return bad(err, "dt must be positive and finite");
+    if (c->codec != OOCS_CODEC_IDENTITY && c->codec != OOCS_CODEC_BLOCKQUANT) return bad(err, "unknown codec");
+    if (c->codec == OOCS_CODEC_BLOCKQUANT && (c->rate_bits < 2 || c->rate_bits > 24))
+        return bad(err, "BlockQuant rate_bits must be in [2, 24] (q = rate-1 code bits)");
+    if (c->mode < OOCS_MODE_BASELINE || c->mode > OOCS_MODE_COMPRESS_DWB) return bad(err, "unknown mode");
+    if (c->mode == OOCS_MODE_BASELINE && c->codec != OOCS_CODEC_IDENTITY)
+        return bad(err, "BASELINE mode (fig:3ver(a)) moves uncompressed data: codec must be identity");
+    if (c->store != OOCS_STORE_HOST && c->store != OOCS_STORE_DEVICE) return bad(err, "unknown store kind");
+    if (c->store == OOCS_STORE_HOST && !c->region_sharing)
+        return bad(err, "an in-place host store requires region sharing (the overlap of chunk i+1 is overwritten "
+                        "by chunk i's write-back; SURVEY §8(a) a3)");
+    if (c->n_blocks < 1 || c->tb_depth < 1) return bad(err, "n_blocks and tb_depth must be >= 1");
+    if (c->nz / 4 < c->n_blocks) return bad(err, "more chunks than 4-plane units: empty chunk (S:L57)");
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad(err, "bad rank/world");
+    if (c->n_blocks % c->world) return bad(err, "world must divide n_blocks (whole chunks per GPU)");
+    if (c->device < 0) return bad(err, "bad device ordinal");
+    return true;
+}
+
+oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err) {
+    if (!validate(cfg, err)) return OOCS_ERR_CONFIG;
+    const oocs_config &c = *cfg;
+    g->cfg = c;
+    g->nx = c.nx;
+    g->ny = c.ny;
+    g->nz = c.nz;
+    g->ax = c.nx + 2 * R;
+    g->ay = c.ny + 2 * R;
+    g->az = c.nz + 2 * R;
+    g->pitch = (XOFF + g->ax + 31) / 32 * 32;
+    g->pstride = g->ay * g->pitch;
+    g->codec = c.codec;
+    g->q = c.codec == OOCS_CODEC_BLOCKQUANT ? c.rate_bits - 1 : 0;
+    g->plane_bytes = c.codec == OOCS_CODEC_BLOCKQUANT ? (g->ax / 4) * (g->ay / 4) * 8 * (g->q + 1) / 4
+                                                      : g->ax * g->ay * 4;
+    g->k = c.tb_depth;
+    const int n = c.n_blocks;
+    const int64_t kR = (int64_t)c.tb_depth * R;
+    // owned planes: 4-plane units, remainder to the leading chunks (Q5)
+    const int64_t units = c.nz / 4, base = units / n, rem = units % n;
+    g->blocks.assign(n, oocs_block{});
+    int64_t lo = 0;
+    for (int i = 0; i < n; ++i) {
+        const int64_t w = 4 * (base + (i < rem ? 1 : 0));
+        if (kR >= w) {
+            if (err) *err = "k*R must be smaller than every chunk's owned width (S:L57)";
+            return OOCS_ERR_CONFIG;
+        }
+        oocs_block &b = g->blocks[i];
+        b.own_lo = lo;
+        b.own_hi = lo + w;
+        b.ext_lo = std::max<int64_t>(-R, b.own_lo - kR);
+        b.ext_hi = std::min<int64_t>(c.nz + R, b.own_hi + kR);
+        // the previous chunk's extent reaches own_lo + kR: that overlap stays on the GPU
+        if (i > 0 && c.region_sharing) {
+            b.carry_lo = b.own_lo - kR;
+            b.carry_hi = b.own_lo + kR;
+        } else {
+            b.carry_lo = b.carry_hi = b.ext_lo;
+        }
+        b.body_lo = b.carry_hi;
+        b.body_hi = b.ext_hi;
+        lo = b.own_hi;
+    }
+    g->b_lo = (int)((int64_t)c.rank * n / c.world);
+    g->b_hi = (int)((int64_t)(c.rank + 1) * n / c.world);
+    g->store_lo = std::max<int64_t>(-R, g->blocks[g->b_lo].own_lo - kR);
+    g->store_hi = std::min<int64_t>(c.nz + R, g->blocks[g->b_hi - 1].own_hi + kR);
+    g->max_ext = g->max_own = 0;
+    for (int i = g->b_lo; i < g->b_hi; ++i) {
+        g->max_ext = std::max(g->max_ext, g->blocks[i].ext_hi - g->blocks[i].ext_lo);
+        g->max_own = std::max(g->max_own, g->blocks[i].own_hi - g->blocks[i].own_lo);
+    }
+    g->host_store = c.store == OOCS_STORE_HOST;
+    if (!g->host_store)
+        g->n_ws = 1;
+    else
+        g->n_ws = c.mode == OOCS_MODE_COMPRESS_SWB ? 1 : c.mode == OOCS_MODE_COMPRESS_DWB ? 2 : 3;
+    return OOCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Lowering.  g = global block counter (sweep * nb + local block), lane
+// s(g) = g mod 3 (S:L425 repair of Algorithm 1's never-updated si), working
+// set w(g) = g mod n_ws.  Codec modes follow Algorithm 1 line by line:
+//   iteration g:  [deferred tail of g-1 on lane s(g-1)]
+//                 ENCODE(g-1); RECORD evt_enc(g-1); D2H(g-1); RECORD evt_d2h(g-1)
+//
+//                 [head of g on lane s(g)]
+//                 WAIT evt_d2h of the previous sweep's chunks whose owned planes this
+//                      H2D reads (cross-sweep RAW on the in-place host store, a10)
+//                 WAIT evt_h2d(g-2)   (staging reuse: carry of g-2 read our buffer)
+//                 H2D(g)             (body only: region sharing P:L87)
+//                 WAIT evt_h2d(g-1); CARRY(g)   (overlap copied on the GPU)
+//                 RECORD evt_h2d(g)
+//                 WAIT evt_enc(g - n_ws)         (working-buffer hand-off)
+//                 DECODE(g); RECORD evt_dec(g); STEP(g, 1..k)
+//   drain epilogue after the loop.
+// ---------------------------------------------------------------------------
+namespace {
+struct Emitter {
+    std::vector<oocs_op> &ops;
+    void emit(int kind, int lane, int64_t g, int block, int sweep, int arg = 0, int64_t ev_g = -1) {
+        oocs_op o;
+        std::memset(&o, 0, sizeof(o));
+        o.kind = kind;
+        o.lane = lane;
+        o.g = g;
+        o.block = block;
+        o.sweep = sweep;
+        o.arg = arg;
+        o.ev_g = ev_g;
+        ops.push_back(o);
+    }
+};
+}  // namespace
+
+void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
+    ops.clear();
+    Emitter E{ops};
+    const int nb = geo.nb();
+    const int64_t G = sweeps * nb;
+    const bool multi = geo.cfg.world > 1;
+    if (!geo.host_store) {
+        for (int64_t g = 0; g < G; ++g) {
+            const int t = (int)(g / nb), blk = geo.b_lo + (int)(g % nb);
+            E.emit(OOCS_OP_DECODE, 0, g, blk, t);
+            for (int s = 1; s <= geo.k; ++s) E.emit(OOCS_OP_STEP, 0, g, blk, t, s);
+            E.emit(OOCS_OP_ENCODE, 0, g, blk, t);
+            if (multi && g % nb == nb - 1 && t + 1 < sweeps) E.emit(OOCS_OP_EXCHANGE, 0, g, blk, t);
+        }
+        return;
+    }
+    auto lane = [](int64_t g) { return (int)(g % N_LANES); };
+    auto blk_of = [&](int64_t g) { return geo.b_lo + (int)(g % nb); };
+    // previous sweep's chunks whose owned planes intersect [lo, hi)
+    auto raw_waits = [&](int64_t g, int64_t lo, int64_t hi) {
+        const int t = (int)(g / nb);
+        if (t == 0) return;
+        for (int j = 0; j < nb; ++j) {
+            const oocs_block &b = geo.blocks[geo.b_lo + j];
+            if (b.own_lo < hi && lo < b.own_hi)
+                E.emit(OOCS_OP_WAIT, lane(g), g, blk_of(g), t, OOCS_EV_D2H, (int64_t)(t - 1) * nb + j);
+        }
+    };
+    if (geo.cfg.mode == OOCS_MODE_BASELINE) {
+        // fig:3ver(a): three private working sets, H2D straight into them; the
+        // overlap is copied GPU-side from the previous chunk's working set
+        // before that chunk's compute overwrites it.
+        for (int64_t g = 0; g < G; ++g) {
+            const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
+            const oocs_block &b = geo.blocks[blk];
+            if (multi && i == 0 && t > 0) E.emit(OOCS_OP_EXCHANGE, s, g, blk, t - 1);
+            else raw_waits(g, b.body_lo, b.body_hi);
+            E.emit(OOCS_OP_H2D, s, g, blk, t);
+            if (i > 0) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_CARRY, g);
+            if (i + 1 < nb) {
+                if (g >= 2) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_D2H, g - 2);
+                E.emit(OOCS_OP_CARRY, s, g + 1, blk + 1, t);
+                E.emit(OOCS_OP_RECORD, s, g + 1, blk + 1, t, OOCS_EV_CARRY, g + 1);
+            }
+            for (int st = 1; st <= geo.k; ++st) E.emit(OOCS_OP_STEP, s, g, blk, t, st);
+            E.emit(OOCS_OP_D2H, s, g, blk, t);
+            E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_D2H, g);
+        }
+        return;
+    }
+    int64_t pending = -1;
+    auto tail = [&](int64_t p) {
+        const int s = lane(p), blk = blk_of(p), t = (int)(p / nb);
+        E.emit(OOCS_OP_ENCODE, s, p, blk, t);
+        E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_ENC, p);
+        E.emit(OOCS_OP_D2H, s, p, blk, t);
+        E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_D2H, p);
+    };
+    bool synced = false;  // an EXCHANGE drained every lane: no cross-sweep waits needed
+    for (int64_t g = 0; g < G; ++g) {
+        const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
+        const oocs_block &b = geo.blocks[blk];
+        if (pending >= 0) {
+            tail(pending);
+            pending = -1;
+        }
+        if (!synced) raw_waits(g, b.body_lo, b.body_hi);
+        synced = false;
+        if (g >= 2) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 2);
+        E.emit(OOCS_OP_H2D, s, g, blk, t);
+        if (i > 0 && b.carry_hi > b.carry_lo) {
+            E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 1);
+            E.emit(OOCS_OP_CARRY, s, g, blk, t);
+        }
+        E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_H2D, g);
+        if (g >= geo.n_ws) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_ENC, g - geo.n_ws);
+        E.emit(OOCS_OP_DECODE, s, g, blk, t);
+        E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_DEC, g);
+        for (int st = 1; st <= geo.k; ++st) E.emit(OOCS_OP_STEP, s, g, blk, t, st);
+        pending = g;
+        if (multi && i == nb - 1 && t + 1 < sweeps) {
+            tail(pending);
+            pending = -1;
+            E.emit(OOCS_OP_EXCHANGE, s, g, blk, t);
+            synced = true;
+        }
+    }
+    if (pending >= 0) tail(pending);  // drain epilogue
+}
+
+}  // namespace oocs
+
+using namespace oocs;
+
+extern "C" oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out) {
+    Geometry g;
+    std::string err;
+    oocs_status st = make_geometry(cfg, &g, &err);
+    if (st != OOCS_OK) {
+        set_error(err);
+        return st;
+    }
+    if (out) std::memcpy(out, g.blocks.data(), g.blocks.size() * sizeof(oocs_block));
+    return OOCS_OK;
+}
+
+extern "C" oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs_op *ops, int64_t cap,
+                                     int64_t *n_ops) {
+    Geometry g;
+    std::string err;
+    oocs_status st = make_geometry(cfg, &g, &err);
+    if (st != OOCS_OK) {
+        set_error(err);
+        return st;
+    }
+    if (steps < 0 || steps % g.k) {
+        set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
+        return OOCS_ERR_CONFIG;
+    }
+    std::vector<oocs_op> v;
+    lower_schedule(g, steps / g.k, v);
+    if (n_ops) *n_ops = (int64_t)v.size();
+    if (ops && cap > 0) std::memcpy(ops, v.data(), std::min<int64_t>(cap, (int64_t)v.size()) * sizeof(oocs_op));
+    return OOCS_OK;
+}
+
+extern "C" oocs_status oocs_encoded_bytes(const oocs_config *cfg, int64_t planes, uint64_t *bytes) {
+    Geometry g;
+    std::string err;
+    oocs_status st = make_geometry(cfg, &g, &err);
+    if (st != OOCS_OK) {
+        set_error(err);
+        return st;
+    }
+    if (planes < 0 || planes % 4) {
+        set_error("planes must be a non-negative multiple of 4");
+        return OOCS_ERR_CONFIG;
+    }
+    if (bytes) *bytes = (uint64_t)(planes * g.plane_bytes);
+    return OOCS_OK;
+}

@@ -1,0 +1,780 @@
+// Plan lifetime, device arena ("single working buffer" allocator), pinned
+// compressed host store, and the stream/event executor of the lowered
+// Algorithm-1 schedule (plan.cpp).  C ABI: include/oocs.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "oocs_internal.h"
+
+namespace oocs {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+struct Arena {
+    char *base = nullptr;
+    size_t cap = 0, used = 0;
+    bool owned = false;
+    void *take(size_t bytes) {
+        const size_t off = (used + 255) & ~size_t(255);
+        if (off + bytes > cap) return nullptr;
+        used = off + bytes;
+        return base + off;
+    }
+};
+
+struct KernelTiming {
+    int kind;  // 0 decode, 1 step, 2 encode
+    cudaEvent_t a, b;
+};
+
+struct Plan {
+    Geometry geo;
+    Arena arena;
+    uint64_t arena_bytes = 0, ws_bytes = 0, staging_bytes = 0, store_bytes = 0;
+    float *ws[3][N_ARRAYS] = {};     // working sets (fl_buf); [set][array]
+    uint8_t *hf_in[N_LANES] = {};    // compressed in-staging per lane: 3 arrays x max_ext planes
+    uint8_t *hf_out[N_LANES] = {};   // compressed out-staging per lane: 2 arrays x max_own planes
+    uint8_t *dstore[2][N_ARRAYS] = {};  // device store (double-buffered pressures; velocity once)
+    int cur = 0;
+    uint8_t *hstore[N_ARRAYS] = {};  // pinned host store, store_planes x plane_bytes per array
+    uint8_t *xbuf[4] = {};           // exchange buffers: send_lo, send_hi, recv_lo, recv_hi
+    uint64_t xbytes = 0;
+    int *d_err = nullptr;
+    cudaStream_t lanes[N_LANES] = {};
+    std::vector<cudaEvent_t> ev[5];
+    int ev_ring = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[N_LANES] = {};
+    oocs_exchange_fn xfn = nullptr;
+    void *xuser = nullptr;
+    bool poisoned = false;
+    std::vector<KernelTiming> timing_pool;
+    size_t timing_used = 0;
+};
+
+}  // namespace oocs
+
+// the opaque ABI handle is the plan itself
+struct oocs_plan : public oocs::Plan {};
+
+namespace oocs {
+
+#define CU(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(e_));             \
+            return OOCS_ERR_CUDA;                                                      \
+        }                                                                              \
+    } while (0)
+
+static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------
+// helpers on the geometry
+// ---------------------------------------------------------------------------
+static inline uint64_t pb(const Plan *p) { return (uint64_t)p->geo.plane_bytes; }
+// byte offset of interior plane z inside one array of the host store
+static inline uint64_t hoff(const Plan *p, int64_t z) { return (uint64_t)(z - p->geo.store_lo) * pb(p); }
+// device store: same indexing
+static inline float *wsa(Plan *p, int set, int a) { return p->ws[set][a]; }
+
+static cudaEvent_t evt(Plan *p, int kind, int64_t g) { return p->ev[kind][(size_t)(g % p->ev_ring)]; }
+
+static oocs_status poison(Plan *p, oocs_status st) {
+    if (st == OOCS_ERR_CUDA) p->poisoned = true;
+    return st;
+}
+
+// pitched 2D copy of `planes` allocated planes between raw (row = ax floats)
+// and working-buffer layout
+static cudaError_t copy_raw_to_ws(float *ws_plane0, const void *raw, const Geometry &g, int64_t planes,
+                                  cudaMemcpyKind kind, cudaStream_t st) {
+    return cudaMemcpy2DAsync(ws_plane0 + XOFF, g.pitch * 4, raw, g.ax * 4, g.ax * 4, planes * g.ay, kind, st);
+}
+static cudaError_t copy_ws_to_raw(void *raw, const float *ws_plane0, const Geometry &g, int64_t planes,
+                                  cudaMemcpyKind kind, cudaStream_t st) {
+    return cudaMemcpy2DAsync(raw, g.ax * 4, ws_plane0 + XOFF, g.pitch * 4, g.ax * 4, planes * g.ay, kind, st);
+}
+
+// ---------------------------------------------------------------------------
+// kernel launch wrappers with optional event timing
+// ---------------------------------------------------------------------------
+static KernelTiming *timing_slot(Plan *p, int kind) {
+    if (!(p->geo.cfg.flags & OOCS_FLAG_PROFILE)) return nullptr;
+    if (p->timing_used == p->timing_pool.size()) {
+        KernelTiming t{kind, nullptr, nullptr};
+        if (cudaEventCreate(&t.a) != cudaSuccess || cudaEventCreate(&t.b) != cudaSuccess) return nullptr;
+        p->timing_pool.push_back(t);
+    }
+    KernelTiming *t = &p->timing_pool[p->timing_used++];
+    t->kind = kind;
+    return t;
+}
+
+static oocs_status k_decode(Plan *p, const void *src, float *dst, int64_t planes, cudaStream_t st,
+                            oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 0);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_decode(src, dst, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[0]++;
+        const uint64_t vals = (uint64_t)planes * p->geo.ax * p->geo.ay;
+        stats->alg_bytes[0] += (uint64_t)planes * pb(p) + vals * 4;
+    }
+    return OOCS_OK;
+}
+
+static oocs_status k_encode(Plan *p, const float *src, void *dst, int64_t planes, cudaStream_t st,
+                            oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 2);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_encode(src, dst, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, p->d_err, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[2]++;
+        const uint64_t vals = (uint64_t)planes * p->geo.ax * p->geo.ay;
+        stats->alg_bytes[2] += vals * 4 + (uint64_t)planes * pb(p);
+    }
+    return OOCS_OK;
+}
+
+static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, int64_t zlo, int64_t zhi,
+                          cudaStream_t st, oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 1);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_step(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, zlo, zhi, p->geo.cfg.dt, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[1]++;
+        const uint64_t cells = (uint64_t)(zhi - zlo) * p->geo.nx * p->geo.ny;
+        stats->cell_updates_computed += cells;
+        stats->alg_bytes[1] += cells * 16;  // read p_curr, p_prev, v; write p_next
+    }
+    return OOCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan create / destroy
+// ---------------------------------------------------------------------------
+static void free_plan(Plan *p) {
+    if (!p) return;
+    int cur_dev = -1;
+    cudaGetDevice(&cur_dev);
+    cudaSetDevice(p->geo.cfg.device);
+    for (auto &s : p->lanes)
+        if (s) cudaStreamDestroy(s);
+    for (auto &v : p->ev)
+        for (auto e : v) cudaEventDestroy(e);
+    for (auto e : p->lane_done)
+        if (e) cudaEventDestroy(e);
+    if (p->t0) cudaEventDestroy(p->t0);
+    if (p->t1) cudaEventDestroy(p->t1);
+    for (auto &t : p->timing_pool) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    if (p->arena.owned && p->arena.base) cudaFree(p->arena.base);
+    for (auto h : p->hstore)
+        if (h) cudaFreeHost(h);
+    if (cur_dev >= 0) cudaSetDevice(cur_dev);
+    delete static_cast<oocs_plan *>(p);
+}
+
+static oocs_status create(const oocs_config *cfg, Plan **out) {
+    *out = nullptr;
+    oocs_plan *p = new (std::nothrow) oocs_plan();
+    if (!p) return OOCS_ERR_HOST_OOM;
+    std::string err;
+    oocs_status st = make_geometry(cfg, &p->geo, &err);
+    if (st != OOCS_OK) {
+        set_error(err);
+        delete p;
+        return st;
+    }
+    const Geometry &g = p->geo;
+    CU(cudaSetDevice(g.cfg.device));
+    // ---- arena sizing ("single working buffer" allocator) ----
+    const size_t ws_array = (size_t)g.max_ext * g.pstride * 4;
+    p->ws_bytes = N_ARRAYS * al(ws_array);
+    size_t total = g.n_ws * p->ws_bytes;
+    const bool codec_staging = g.host_store && g.cfg.mode != OOCS_MODE_BASELINE;
+    size_t hin = 0, hout = 0;
+    if (codec_staging) {
+        hin = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
+        hout = al((size_t)2 * g.max_own * g.plane_bytes);
+        p->staging_bytes = N_LANES * (hin + hout);
+        total += p->staging_bytes;
+    }
+    const size_t arr_store = (size_t)g.store_planes() * g.plane_bytes;
+    p->store_bytes = N_ARRAYS * arr_store;
+    if (!g.host_store) total += al(arr_store) * 5;  // v + 2x(p_prev, p_curr)
+    const int64_t kR = (int64_t)g.k * R;
+    if (g.cfg.world > 1) {
+        p->xbytes = (uint64_t)2 * kR * g.plane_bytes;
+        total += 4 * al(p->xbytes);
+    }
+    total += 256;  // error flag
+    p->arena_bytes = total;
+    if (g.cfg.device_capacity && total > g.cfg.device_capacity) {
+        set_error("device arena (" + std::to_string(total) + " B) exceeds device_capacity");
+        delete p;
+        return OOCS_ERR_DEVICE_OOM;
+    }
+    cudaError_t ce = cudaMalloc((void **)&p->arena.base, total);
+    if (ce != cudaSuccess) {
+        cudaGetLastError();
+        set_error(std::string("cudaMalloc of the device arena failed: ") + cudaGetErrorString(ce));
+        delete p;
+        return OOCS_ERR_DEVICE_OOM;
+    }
+    p->arena.cap = total;
+    p->arena.owned = true;
+    for (int s = 0; s < g.n_ws; ++s)
+        for (int a = 0; a < N_ARRAYS; ++a) p->ws[s][a] = (float *)p->arena.take(ws_array);
+    if (codec_staging)
+        for (int l = 0; l < N_LANES; ++l) {
+            p->hf_in[l] = (uint8_t *)p->arena.take(hin);
+            p->hf_out[l] = (uint8_t *)p->arena.take(hout);
+        }
+    if (!g.host_store) {
+        p->dstore[0][0] = (uint8_t *)p->arena.take(arr_store);
+        p->dstore[1][0] = p->dstore[0][0];
+        for (int b = 0; b < 2; ++b)
+            for (int a = 1; a < N_ARRAYS; ++a) p->dstore[b][a] = (uint8_t *)p->arena.take(arr_store);
+    }
+    if (g.cfg.world > 1)
+        for (int i = 0; i < 4; ++i) p->xbuf[i] = (uint8_t *)p->arena.take(p->xbytes);
+    p->d_err = (int *)p->arena.take(sizeof(int));
+    if (!p->d_err) {
+        set_error("internal: arena carve-out overflow");
+        free_plan(p);
+        return OOCS_ERR_STATE;
+    }
+    // zero the working sets so halo columns / padding are defined
+    if (cudaMemset(p->arena.base, 0, total) != cudaSuccess) {
+        set_error("cudaMemset of the arena failed");
+        free_plan(p);
+        return OOCS_ERR_CUDA;
+    }
+    if (g.host_store) {
+        for (int a = 0; a < N_ARRAYS; ++a) {
+            ce = cudaHostAlloc((void **)&p->hstore[a], std::max<size_t>(arr_store, 1), cudaHostAllocDefault);
+            if (ce != cudaSuccess) {
+                cudaGetLastError();
+                set_error(std::string("pinned host store allocation failed: ") + cudaGetErrorString(ce));
+                free_plan(p);
+                return OOCS_ERR_HOST_OOM;
+            }
+            std::memset(p->hstore[a], 0, arr_store);
+        }
+    }
+    for (int l = 0; l < N_LANES; ++l) {
+        if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->lane_done[l], cudaEventDisableTiming) != cudaSuccess) {
+            set_error("stream/event creation failed");
+            free_plan(p);
+            return OOCS_ERR_CUDA;
+        }
+    }
+    p->ev_ring = g.nb() + 8;
+    for (int k = 0; k < 5; ++k) {
+        p->ev[k].resize(p->ev_ring);
+        for (auto &e : p->ev[k])
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                set_error("event creation failed");
+                free_plan(p);
+                return OOCS_ERR_CUDA;
+            }
+    }
+    if (cudaEventCreate(&p->t0) != cudaSuccess || cudaEventCreate(&p->t1) != cudaSuccess) {
+        set_error("event creation failed");
+        free_plan(p);
+        return OOCS_ERR_CUDA;
+    }
+    *out = p;
+    return OOCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// executor
+// ---------------------------------------------------------------------------
+// STEP s updates array (s odd ? 1 : 2) from the other one (leapfrog in place).
+static inline int upd_array(int s) { return (s & 1) ? 1 : 2; }
+
+static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
+    const Geometry &g = p->geo;
+    const int64_t kR = (int64_t)g.k * R;
+    const int64_t Zlo = g.blocks[g.b_lo].own_lo, Zhi = g.blocks[g.b_hi - 1].own_hi;
+    const bool has_lo = g.cfg.rank > 0, has_hi = g.cfg.rank + 1 < g.cfg.world;
+    for (auto s : p->lanes) CU(cudaStreamSynchronize(s));
+    cudaStream_t st = p->lanes[0];
+    const uint64_t arr = (uint64_t)kR * pb(p);
+    // pack: planes [Zlo, Zlo+kR) -> send_lo ; [Zhi-kR, Zhi) -> send_hi ; arrays 1, 2
+    for (int a = 1; a <= 2; ++a) {
+        const uint64_t o = (uint64_t)(a - 1) * arr;
+        if (g.host_store) {
+            if (has_lo) CU(cudaMemcpyAsync(p->xbuf[0] + o, p->hstore[a] + hoff(p, Zlo), arr, cudaMemcpyHostToDevice, st));
+            if (has_hi) CU(cudaMemcpyAsync(p->xbuf[1] + o, p->hstore[a] + hoff(p, Zhi - kR), arr, cudaMemcpyHostToDevice, st));
+        } else {
+            uint8_t *S = p->dstore[p->cur ^ 1][a];
+            if (has_lo) CU(cudaMemcpyAsync(p->xbuf[0] + o, S + hoff(p, Zlo), arr, cudaMemcpyDeviceToDevice, st));
+            if (has_hi) CU(cudaMemcpyAsync(p->xbuf[1] + o, S + hoff(p, Zhi - kR), arr, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    CU(cudaStreamSynchronize(st));
+    if (!p->xfn) {
+        set_error("world > 1 but no exchange callback installed (oocs_set_exchange)");
+        return OOCS_ERR_EXCHANGE;
+    }
+    const int rc = p->xfn(p->xuser, sweep, has_lo ? p->xbuf[0] : nullptr, has_hi ? p->xbuf[1] : nullptr,
+                          has_lo ? p->xbuf[2] : nullptr, has_hi ? p->xbuf[3] : nullptr, p->xbytes, (void *)st);
+    if (rc) {
+        set_error("halo exchange callback failed");
+        return OOCS_ERR_EXCHANGE;
+    }
+    // unpack: recv_lo -> ghost planes [Zlo-kR, Zlo) ; recv_hi -> [Zhi, Zhi+kR)
+    for (int a = 1; a <= 2; ++a) {
+        const uint64_t o = (uint64_t)(a - 1) * arr;
+        if (g.host_store) {
+            if (has_lo) CU(cudaMemcpyAsync(p->hstore[a] + hoff(p, Zlo - kR), p->xbuf[2] + o, arr, cudaMemcpyDeviceToHost, st));
+            if (has_hi) CU(cudaMemcpyAsync(p->hstore[a] + hoff(p, Zhi), p->xbuf[3] + o, arr, cudaMemcpyDeviceToHost, st));
+        } else {
+            uint8_t *S = p->dstore[p->cur ^ 1][a];
+            if (has_lo) CU(cudaMemcpyAsync(S + hoff(p, Zlo - kR), p->xbuf[2] + o, arr, cudaMemcpyDeviceToDevice, st));
+            if (has_hi) CU(cudaMemcpyAsync(S + hoff(p, Zhi), p->xbuf[3] + o, arr, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    CU(cudaStreamSynchronize(st));
+    if (stats) stats->bytes_exchange += (uint64_t)(has_lo + has_hi) * p->xbytes;
+    return OOCS_OK;
+}
+
+static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats *stats) {
+    const Geometry &g = p->geo;
+    const int64_t kR = (int64_t)g.k * R;
+    const uint64_t PB = pb(p);
+    const int nb = g.nb();
+    auto blk = [&](const oocs_op &o) -> const oocs_block & { return g.blocks[o.block]; };
+    for (const oocs_op &o : ops) {
+        cudaStream_t st = p->lanes[o.lane];
+        const oocs_block &b = blk(o);
+        const int64_t E = b.ext_hi - b.ext_lo;
+        const int w = (int)(o.g % g.n_ws);
+        const int s = (int)(o.g % N_LANES);
+        switch (o.kind) {
+        case OOCS_OP_WAIT:
+            CU(cudaStreamWaitEvent(st, evt(p, o.arg, o.ev_g), 0));
+            break;
+        case OOCS_OP_RECORD:
+            CU(cudaEventRecord(evt(p, o.arg, o.ev_g), st));
+            break;
+        case OOCS_OP_H2D: {
+            const int64_t nplanes = b.body_hi - b.body_lo, off = b.body_lo - b.ext_lo;
+            if (g.cfg.mode == OOCS_MODE_BASELINE) {
+                for (int a = 0; a < N_ARRAYS; ++a)
+                    CU(copy_raw_to_ws(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), g, nplanes,
+                                      cudaMemcpyHostToDevice, st));
+            } else {
+                for (int a = 0; a < N_ARRAYS; ++a)
+                    CU(cudaMemcpyAsync(p->hf_in[s] + ((uint64_t)a * g.max_ext + off) * PB,
+                                       p->hstore[a] + hoff(p, b.body_lo), nplanes * PB, cudaMemcpyHostToDevice, st));
+            }
+            if (stats) stats->bytes_h2d += (uint64_t)N_ARRAYS * nplanes * PB;
+            break;
+        }
+        case OOCS_OP_CARRY: {
+            // overlap of this chunk with the previous chunk's extent, already on the GPU
+            const oocs_block &pbk = g.blocks[o.block - 1];
+            const int64_t nplanes = b.carry_hi - b.carry_lo;
+            const int64_t src_off = b.carry_lo - pbk.ext_lo, dst_off = b.carry_lo - b.ext_lo;
+            if (g.cfg.mode == OOCS_MODE_BASELINE) {
+                // lane of o is the previous chunk's lane; destination is chunk g's working set
+                const int wprev = (int)((o.g - 1) % g.n_ws);
+                for (int a = 0; a < N_ARRAYS; ++a)
+                    CU(cudaMemcpy2DAsync(wsa(p, w, a) + dst_off * g.pstride, g.pitch * 4,
+                                         wsa(p, wprev, a) + src_off * g.pstride, g.pitch * 4, g.pitch * 4,
+                                         nplanes * g.ay, cudaMemcpyDeviceToDevice, st));
+                if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
+            } else {
+                const int sp = (int)((o.g - 1) % N_LANES);
+                for (int a = 0; a < N_ARRAYS; ++a)
+                    CU(cudaMemcpyAsync(p->hf_in[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
+                                       p->hf_in[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
+                                       cudaMemcpyDeviceToDevice, st));
+                if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * PB;
+            }
+            break;
+        }
+        case OOCS_OP_DECODE: {
+            for (int a = 0; a < N_ARRAYS; ++a) {
+                const uint8_t *src;
+                if (g.host_store)
+                    src = p->hf_in[s] + (uint64_t)a * g.max_ext * PB;
+                else
+                    src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
+                oocs_status r = k_decode(p, src, wsa(p, w, a), E, st, stats);
+                if (r) return r;
+            }
+            break;
+        }
+        case OOCS_OP_STEP: {
+            // step s is valid on [lo_s, hi_s): the trapezoid shrinks by R per step except at
+            // the physical boundary (P:L85 temporal blocking)
+            const int sidx = o.arg;
+            const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
+            const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
+            const int up = upd_array(sidx), other = 3 - up;
+            oocs_status r = k_step(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo, st,
+                                   stats);
+            if (r) return r;
+            break;
+        }
+        case OOCS_OP_ENCODE: {
+            // after k steps: level t0+k in array upd(k), level t0+k-1 in the other
+            const int curr = upd_array(g.k), prev = 3 - curr;
+            const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;
+            const int src_arr[2] = {prev, curr};
+            for (int j = 0; j < 2; ++j) {
+                void *dst;
+                if (g.host_store)
+                    dst = p->hf_out[s] + (uint64_t)j * g.max_own * PB;
+                else
+                    dst = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
+                oocs_status r = k_encode(p, wsa(p, w, src_arr[j]) + off * g.pstride, dst, W, st, stats);
+                if (r) return r;
+            }
+            break;
+        }
+        case OOCS_OP_D2H: {
+            const int64_t W = b.own_hi - b.own_lo;
+            if (g.cfg.mode == OOCS_MODE_BASELINE) {
+                const int curr = upd_array(g.k), prev = 3 - curr;
+                const int64_t off = b.own_lo - b.ext_lo;
+                CU(copy_ws_to_raw(p->hstore[1] + hoff(p, b.own_lo), wsa(p, w, prev) + off * g.pstride, g, W,
+                                  cudaMemcpyDeviceToHost, st));
+                CU(copy_ws_to_raw(p->hstore[2] + hoff(p, b.own_lo), wsa(p, w, curr) + off * g.pstride, g, W,
+                                  cudaMemcpyDeviceToHost, st));
+            } else {
+                for (int j = 0; j < 2; ++j)
+                    CU(cudaMemcpyAsync(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf_out[s] + (uint64_t)j * g.max_own * PB,
+                                       W * PB, cudaMemcpyDeviceToHost, st));
+            }
+            if (stats) stats->bytes_d2h += (uint64_t)2 * W * PB;
+            break;
+        }
+        case OOCS_OP_EXCHANGE: {
+            oocs_status r = do_exchange(p, o.sweep, stats);
+            if (r) return r;
+            if (!g.host_store) p->cur ^= 1;
+            break;
+        }
+        default:
+            set_error("internal: unknown op");
+            return OOCS_ERR_STATE;
+        }
+        // device store: the sweep ends after the last chunk's ENCODE (single lane, in order)
+        if (!g.host_store && o.kind == OOCS_OP_ENCODE && o.g % nb == nb - 1) {
+            const bool exch_follows = g.cfg.world > 1 && (&o != &ops.back()) && (&o + 1)->kind == OOCS_OP_EXCHANGE;
+            if (!exch_follows) p->cur ^= 1;
+        }
+    }
+    (void)kR;
+    return OOCS_OK;
+}
+
+static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
+    const Geometry &g = p->geo;
+    if (steps < 0 || steps % g.k) {
+        set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
+        return OOCS_ERR_CONFIG;
+    }
+    if (g.cfg.world > 1 && !p->xfn) {
+        set_error("world > 1 requires oocs_set_exchange");
+        return OOCS_ERR_STATE;
+    }
+    CU(cudaSetDevice(g.cfg.device));
+    oocs_stats stats;
+    std::memset(&stats, 0, sizeof(stats));
+    std::vector<oocs_op> ops;
+    lower_schedule(g, steps / g.k, ops);
+    p->timing_used = 0;
+    CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->lanes[0]));
+    CU(cudaEventRecord(p->t0, p->lanes[0]));
+    for (int l = 1; l < N_LANES; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0, 0));
+    oocs_status st = execute(p, ops, &stats);
+    if (st) return poison(p, st);
+    for (int l = 1; l < N_LANES; ++l) {
+        CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
+        CU(cudaStreamWaitEvent(p->lanes[0], p->lane_done[l], 0));
+    }
+    CU(cudaEventRecord(p->t1, p->lanes[0]));
+    CU(cudaEventSynchronize(p->t1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, p->t0, p->t1));
+    stats.wall_ms = ms;
+    for (size_t i = 0; i < p->timing_used; ++i) {
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, p->timing_pool[i].a, p->timing_pool[i].b));
+        stats.kernel_ms[p->timing_pool[i].kind] += t;
+    }
+    int herr = 0;
+    CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    stats.data_error = herr;
+    int64_t owned = 0;
+    for (int i = g.b_lo; i < g.b_hi; ++i) owned += g.blocks[i].own_hi - g.blocks[i].own_lo;
+    stats.cell_updates = (uint64_t)g.nx * g.ny * owned * steps;
+    if (out) *out = stats;
+    if (herr) {
+        set_error("encoder rejected a non-finite or |x| >= 2^126 value (S:L200)");
+        return OOCS_ERR_DATA;
+    }
+    return OOCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// load / store
+// ---------------------------------------------------------------------------
+static oocs_status check_range(const Plan *p, int32_t array, int64_t a_lo, int64_t a_hi) {
+    const Geometry &g = p->geo;
+    if (array < 0 || array >= N_ARRAYS) {
+        set_error("array must be 0 (velocity), 1 (p_prev) or 2 (p_curr)");
+        return OOCS_ERR_CONFIG;
+    }
+    if (a_lo < g.a_store_lo() || a_hi > g.a_store_lo() + g.store_planes() || a_lo > a_hi || a_lo % 4 || a_hi % 4) {
+        set_error("plane range outside this rank's store or not 4-aligned");
+        return OOCS_ERR_CONFIG;
+    }
+    return OOCS_OK;
+}
+
+static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
+    oocs_status st = check_range(p, array, a_lo, a_hi);
+    if (st) return st;
+    const Geometry &g = p->geo;
+    CU(cudaSetDevice(g.cfg.device));
+    cudaStream_t s = p->lanes[0];
+    const int64_t chunk = g.max_ext / 4 * 4;
+    float *ws = p->ws[0][0];
+    CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), s));
+    // staging for the compressed result (host store): reuse a slice of ws[0][1]
+    uint8_t *stage = reinterpret_cast<uint8_t *>(p->ws[0][1]);
+    for (int64_t a = a_lo; a < a_hi; a += chunk) {
+        const int64_t n = std::min(chunk, a_hi - a);
+        CU(copy_raw_to_ws(ws, src + (a - a_lo) * g.ax * g.ay, g, n, cudaMemcpyHostToDevice, s));
+        const int64_t z = a - R;
+        if (g.host_store) {
+            oocs_status r = k_encode(p, ws, stage, n, s, nullptr);
+            if (r) return r;
+            CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), stage, n * pb(p), cudaMemcpyDeviceToHost, s));
+        } else {
+            for (int b = 0; b < (array == 0 ? 1 : 2); ++b) {
+                oocs_status r = k_encode(p, ws, p->dstore[b][array] + hoff(p, z), n, s, nullptr);
+                if (r) return r;
+            }
+        }
+        CU(cudaStreamSynchronize(s));
+    }
+    int herr = 0;
+    CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (herr) {
+        set_error("oocs_load: non-finite or |x| >= 2^126 value for a lossy codec (S:L200)");
+        return OOCS_ERR_DATA;
+    }
+    return OOCS_OK;
+}
+
+static oocs_status store(Plan *p, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
+    oocs_status st = check_range(p, array, a_lo, a_hi);
+    if (st) return st;
+    const Geometry &g = p->geo;
+    CU(cudaSetDevice(g.cfg.device));
+    cudaStream_t s = p->lanes[0];
+    const int64_t chunk = g.max_ext / 4 * 4;
+    float *ws = p->ws[0][0];
+    uint8_t *stage = reinterpret_cast<uint8_t *>(p->ws[0][1]);
+    for (int64_t a = a_lo; a < a_hi; a += chunk) {
+        const int64_t n = std::min(chunk, a_hi - a);
+        const int64_t z = a - R;
+        const void *src;
+        if (g.host_store) {
+            CU(cudaMemcpyAsync(stage, p->hstore[array] + hoff(p, z), n * pb(p), cudaMemcpyHostToDevice, s));
+            src = stage;
+        } else {
+            src = p->dstore[array == 0 ? 0 : p->cur][array] + hoff(p, z);
+        }
+        oocs_status r = k_decode(p, src, ws, n, s, nullptr);
+        if (r) return r;
+        CU(copy_ws_to_raw(dst + (a - a_lo) * g.ax * g.ay, ws, g, n, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    return OOCS_OK;
+}
+
+static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int64_t a_hi, bool write) {
+    oocs_status st = check_range(p, array, a_lo, a_hi);
+    if (st) return st;
+    const Geometry &g = p->geo;
+    CU(cudaSetDevice(g.cfg.device));
+    const uint64_t off = hoff(p, a_lo - R), n = (uint64_t)(a_hi - a_lo) * pb(p);
+    if (g.host_store) {
+        if (write)
+            std::memcpy(p->hstore[array] + off, host, n);
+        else
+            std::memcpy(host, p->hstore[array] + off, n);
+        return OOCS_OK;
+    }
+    if (write) {
+        for (int b = 0; b < (array == 0 ? 1 : 2); ++b)
+            CU(cudaMemcpy(p->dstore[b][array] + off, host, n, cudaMemcpyHostToDevice));
+    } else {
+        CU(cudaMemcpy(host, p->dstore[array == 0 ? 0 : p->cur][array] + off, n, cudaMemcpyDeviceToHost));
+    }
+    return OOCS_OK;
+}
+
+}  // namespace oocs
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace oocs;
+
+static oocs_status guard(const oocs_plan *p) {
+    if (!p) {
+        set_error("plan is NULL");
+        return OOCS_ERR_STATE;
+    }
+    if (p->poisoned) {
+        set_error("plan poisoned by an earlier CUDA error; only oocs_destroy is valid");
+        return OOCS_ERR_STATE;
+    }
+    return OOCS_OK;
+}
+
+extern "C" {
+
+oocs_status oocs_plan_create(const oocs_config *cfg, oocs_plan **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return OOCS_ERR_CONFIG;
+    }
+    *out = nullptr;
+    Plan *p = nullptr;
+    oocs_status st = create(cfg, &p);
+    if (st == OOCS_OK) *out = static_cast<oocs_plan *>(p);
+    return st;
+}
+
+oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info) {
+    if (oocs_status st = guard(plan)) return st;
+    if (!info) return OOCS_ERR_CONFIG;
+    const Geometry &g = plan->geo;
+    std::memset(info, 0, sizeof(*info));
+    info->ax = g.ax;
+    info->ay = g.ay;
+    info->az = g.az;
+    info->pitch = g.pitch;
+    info->plane_bytes = g.plane_bytes;
+    info->z_lo = g.blocks[g.b_lo].own_lo;
+    info->z_hi = g.blocks[g.b_hi - 1].own_hi;
+    info->store_lo = g.store_lo;
+    info->store_hi = g.store_hi;
+    info->block_lo = g.b_lo;
+    info->block_hi = g.b_hi;
+    info->max_ext_planes = g.max_ext;
+    info->arena_bytes = plan->arena_bytes;
+    info->working_set_bytes = plan->ws_bytes;
+    info->staging_bytes = plan->staging_bytes;
+    info->store_bytes = plan->store_bytes;
+    info->n_working_sets = g.n_ws;
+    info->n_lanes = N_LANES;
+    return OOCS_OK;
+}
+
+oocs_status oocs_set_exchange(oocs_plan *plan, oocs_exchange_fn fn, void *user) {
+    if (oocs_status st = guard(plan)) return st;
+    plan->xfn = fn;
+    plan->xuser = user;
+    return OOCS_OK;
+}
+
+oocs_status oocs_destroy(oocs_plan *plan) {
+    free_plan(static_cast<Plan *>(plan));
+    return OOCS_OK;
+}
+
+oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, load(plan, array, src, a_lo, a_hi));
+}
+
+oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, store(plan, array, dst, a_lo, a_hi));
+}
+
+oocs_status oocs_store_read_raw(oocs_plan *plan, int32_t array, void *dst, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, raw_io(plan, array, dst, a_lo, a_hi, false));
+}
+
+oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, raw_io(plan, array, const_cast<void *>(src), a_lo, a_hi, true));
+}
+
+oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, run(plan, steps, out));
+}
+
+oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
+                        int32_t codec, int32_t rate_bits, void *stream) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || (codec != 0 && codec != 1) ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24))) {
+        set_error("oocs_decode: bad geometry or codec");
+        return OOCS_ERR_CONFIG;
+    }
+    CU(launch_decode(src, dst, ax, ay, planes, pitch, codec, codec ? rate_bits - 1 : 0, (cudaStream_t)stream));
+    return OOCS_OK;
+}
+
+oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
+                        int32_t codec, int32_t rate_bits, int32_t *err_flag, void *stream) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || (codec != 0 && codec != 1) ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24))) {
+        set_error("oocs_encode: bad geometry or codec");
+        return OOCS_ERR_CONFIG;
+    }
+    int *flag = err_flag;
+    static int *dummy = nullptr;  // per-process scratch flag when the caller passes NULL
+    if (!flag) {
+        if (!dummy) CU(cudaMalloc((void **)&dummy, sizeof(int)));
+        flag = dummy;
+    }
+    CU(launch_encode(src, dst, ax, ay, planes, pitch, codec, codec ? rate_bits - 1 : 0, flag, (cudaStream_t)stream));
+    return OOCS_OK;
+}
+
+oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int64_t ax, int64_t ay, int64_t planes,
+                      int64_t pitch, float dt, int64_t z_lo, int64_t z_hi, void *stream) {
+    if (ax % 4 || ay % 4 || pitch < ax + XOFF || pitch % 32 || z_lo < R || z_hi > planes - R || z_lo > z_hi) {
+        set_error("oocs_step: bad geometry or plane range");
+        return OOCS_ERR_CONFIG;
+    }
+    CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, z_lo, z_hi, dt, (cudaStream_t)stream));
+    return OOCS_OK;
+}
+
+const char *oocs_last_error(void) { return g_last_error.c_str(); }
+int32_t oocs_abi_version(void) { return OOCS_ABI_VERSION; }
+
+}  // extern "C"

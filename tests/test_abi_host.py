@@ -1,0 +1,156 @@
+"""CPU tests of the C-ABI library: symbols, validation, decomposition and the lowered schedule.
+
+No compute calls (no GPU here).  The schedule tests run the exact op list
+oocs_run issues through tests/schedule_check.py: every pair of operations that
+touch the same bytes (one writing) must be ordered by stream order or events
+(SPEC validate_exclusive S:L409-417, acceptance #2 S:L655), Algorithm 1's
+paper-visible sequence must match the hand-unrolled golden file (acceptance #8
+S:L661), and deleting the paper's working-buffer waits must create a race.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2204_11315_b200 as oocs
+import schedule_check as sc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "oocs.h")).read()
+    names = set(re.findall(r"^\s*(?:oocs_status|const char \*|int32_t)\s*(oocs_\w+)\s*\(", hdr, re.M))
+    assert len(names) >= 17
+    L = ctypes.CDLL(oocs.LIB_PATH)
+    for n in sorted(names):
+        assert hasattr(L, n), n
+    assert oocs.lib().oocs_abi_version() == 1
+
+
+def cfg(**kw):
+    base = dict(nx=64, ny=64, nz=64, dt=0.1, n_blocks=4, tb_depth=2)
+    base.update(kw)
+    return oocs.make_config(**base)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(nx=63), dict(nz=0), dict(n_blocks=17), dict(tb_depth=4), dict(rate_bits=25), dict(rate_bits=1),
+    dict(mode="baseline", codec="blockquant"), dict(world=3), dict(rank=4, world=4), dict(dt=-1.0),
+    dict(region_sharing=False, store="host"), dict(codec=7),
+])
+def test_config_errors(kw):
+    with pytest.raises(oocs.OocsError) as e:
+        oocs.oocs_plan_table(cfg(**kw))
+    assert e.value.status == 2
+
+
+def test_struct_size_is_checked():
+    c = cfg()
+    c.struct_size = 8
+    with pytest.raises(oocs.OocsError):
+        oocs.oocs_plan_table(c)
+
+
+@pytest.mark.parametrize("nz,n,k", [(1152, 8, 12), (64, 4, 2), (128, 8, 3), (40, 3, 2), (16, 1, 3), (96, 5, 1)])
+def test_decomposition_matches_oracle(nz, n, k):
+    # the library's planner and the oracle's are written independently
+    got = np.array(oocs.oocs_plan_table(cfg(nz=nz, n_blocks=n, tb_depth=k)))
+    want = oracle.plan(nz, n, k)
+    assert np.array_equal(got, want)
+
+
+def test_encoded_bytes_fixed_rate_law():
+    # rate 16 = half of fp32 (P:L170's 1/2); identity = 4 B/value
+    c16 = cfg(rate_bits=16)
+    c_id = cfg(codec="identity")
+    ax = 72
+    assert oocs.oocs_encoded_bytes(c16, 4) * 2 == oocs.oocs_encoded_bytes(c_id, 4) == 4 * ax * ax * 4
+    for r in (8, 12, 24):
+        assert oocs.oocs_encoded_bytes(cfg(rate_bits=r), 8) == 8 * ax * ax * r // 8
+
+
+def _geo(c, blocks):
+    n_ws = {0: 3, 1: 3, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
+    return dict(k=c.tb_depth, n_ws=n_ws, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz)
+
+
+def _check(c, steps):
+    ops = oocs.oocs_schedule(c, steps)
+    blocks = oocs.oocs_plan_table(c)
+    return ops, sc.violations(ops, blocks, _geo(c, blocks))
+
+
+MODES = [("swb", "blockquant"), ("dwb", "blockquant"), ("compress", "blockquant"), ("baseline", "identity"),
+         ("swb", "identity")]
+
+
+@pytest.mark.parametrize("mode,codec", MODES)
+@pytest.mark.parametrize("n,k,nz", [(1, 1, 16), (2, 1, 32), (3, 2, 48), (4, 2, 64), (5, 3, 80), (8, 1, 64),
+                                    (12, 1, 96)])
+def test_schedule_is_race_free(mode, codec, n, k, nz):
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec)
+    ops, bad = _check(c, 3 * k)  # three sweeps: exercises the cross-sweep host-store hazards
+    assert bad == [], bad[:5]
+    # every chunk of every sweep is decoded/computed/encoded exactly once per step
+    assert sum(o["kind"] == "STEP" for o in ops) == 3 * n * k
+
+
+def test_algorithm1_golden_n3():
+    c = cfg(nz=48, n_blocks=3, tb_depth=1, mode="swb")
+    ops = oocs.oocs_schedule(c, 1)
+    seq = []
+    for o in ops:
+        if o["kind"] in ("H2D", "DECODE", "STEP", "ENCODE", "D2H"):
+            seq.append(f"{o['kind']} {o['lane']} {o['block']}")
+        elif o["kind"] in ("RECORD", "WAIT") and o["ev"] == "ENC":
+            seq.append(f"{o['kind']} {o['lane']} {o['block']} ENC")
+    gold = [l.strip() for l in open(os.path.join(ROOT, "tests", "golden", "alg1_n3.txt"))
+            if l.strip() and not l.startswith("#")]
+    assert seq == gold
+    # lanes cycle 0,1,2,0 and waits connect lanes cyclically 0->1->2
+    c4 = cfg(nz=64, n_blocks=4, tb_depth=1, mode="swb")
+    ops4 = oocs.oocs_schedule(c4, 1)
+    assert [o["lane"] for o in ops4 if o["kind"] == "H2D"] == [0, 1, 2, 0]
+    waits = [(o["lane"], o["ev_g"] % 3) for o in ops4 if o["kind"] == "WAIT" and o["ev"] == "ENC"]
+    assert waits == [(1, 0), (2, 1), (0, 2)]
+
+
+@pytest.mark.parametrize("mode", ["swb", "dwb"])
+def test_deleting_a_working_buffer_wait_creates_a_race(mode):
+    c = cfg(nz=64, n_blocks=4, tb_depth=2, mode=mode)
+    ops = oocs.oocs_schedule(c, 4)
+    blocks = oocs.oocs_plan_table(c)
+    geo = _geo(c, blocks)
+    assert sc.violations(ops, blocks, geo) == []
+    idx = [i for i, o in enumerate(ops) if o["kind"] == "WAIT" and o["ev"] == "ENC"]
+    assert idx
+    for i in idx:
+        mutated = ops[:i] + ops[i + 1:]
+        assert sc.violations(mutated, blocks, geo, limit=1), f"deleting op {i} went unnoticed"
+
+
+def test_deleting_carry_and_cross_sweep_waits_is_detected():
+    c = cfg(nz=64, n_blocks=4, tb_depth=2, mode="swb")
+    ops = oocs.oocs_schedule(c, 4)
+    blocks = oocs.oocs_plan_table(c)
+    geo = _geo(c, blocks)
+    for ev in ("H2D", "D2H"):
+        idx = [i for i, o in enumerate(ops) if o["kind"] == "WAIT" and o["ev"] == ev]
+        caught = sum(bool(sc.violations(ops[:i] + ops[i + 1:], blocks, geo, limit=1)) for i in idx)
+        assert caught >= 1, ev
+
+
+def test_transfer_byte_identities():
+    # region sharing: each interior chunk transfers exactly 2kR planes fewer per dataset
+    for n, k in [(4, 2), (8, 1), (3, 3)]:
+        c = cfg(nz=96, n_blocks=n, tb_depth=k)
+        t = oocs.oocs_plan_table(c)
+        body = sum(b[7] - b[6] for b in t)
+        ext = sum(b[3] - b[2] for b in t)
+        assert ext - body == (n - 1) * 2 * k * oocs.R
+        # and the H2D planes of one sweep cover [-R, nz+R) exactly once
+        assert body == 96 + 2 * oocs.R
