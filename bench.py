@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the out-of-core compressed stencil hot path (arXiv 2204.11315) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl oocs|reference]
+
+One "step" = one oocs_run of the whole hot path over the BASELINE.json configs[1]
+workload (c2: 1024^3 fp32 per GPU, 8 z-chunks, 16 time steps = 4 sweeps of
+temporal depth k=4, BlockQuant rate 16 bits/value, single working buffer):
+every chunk is decompressed, advanced k steps on the shrinking trapezoid and
+recompressed, every sweep.
+
+* value: Gcell-updates/s with the compressed state resident in HBM when the timed
+  region starts (store="device"; no PCIe) -- the kernels' throughput;
+* e2e:   the same metric through the C ABI with the compressed state in pinned HOST
+  memory (store="host", the paper's out-of-core pipeline): H2D of every chunk body,
+  GPU decode / steps / encode, D2H of the owned planes, on 3 streams (Alg. 1).
+N > 1 (torchrun): weak scaling, rank r owns a 1024^3 z-slab of a 1024x1024x(1024N)
+grid; inter-slab halos are exchanged with NCCL after each sweep.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+R = 4
+METRIC = "out-of-core Gcell-updates/s incl. transfers; roofline %; peak GPU memory (GB)"
+UNIT = "Gcell-updates/s"
+WORKLOADS = {
+    # name: (nx, ny, nz per rank, chunks per rank, k, T, rate)
+    "c2": (1024, 1024, 1024, 8, 4, 16, 16),
+    "c1": (64, 64, 64, 4, 2, 4, 16),
+}
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="oocs", choices=["oocs", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+def load_state(plan, nx, ny, nz_global, device):
+    """Generate the synthetic fields slab by slab on the GPU (synth.fields_torch), compress them into
+    the plan's store through oocs_load (outside any timed region)."""
+    import synth
+
+    info = plan.info
+    a_lo, a_hi = info.store_lo + R, info.store_hi + R
+    slab = 64
+    for z0 in range(a_lo, a_hi, slab):
+        z1 = min(a_hi, z0 + slab)
+        v, p = synth.fields_torch(nx, ny, nz_global, z0, z1, device=f"cuda:{device}")
+        v, p = v.cpu().numpy(), p.cpu().numpy()
+        plan.load(0, v, z0, z1)
+        plan.load(1, p, z0, z1)
+        plan.load(2, p, z0, z1)
+
+
+def copy_state(src, dst):
+    a_lo, a_hi = src.info.store_lo + R, src.info.store_hi + R
+    for a in range(3):
+        dst.write_raw(a, src.read_raw(a, a_lo, a_hi), a_lo, a_hi)
+
+
+def timed_runs(plan, T, steps, warmup, barrier, clocks=None):
+    for _ in range(warmup):
+        plan.run(T)
+    barrier()
+    per = []
+    wall0 = time.perf_counter()
+    ctx = clocks if clocks is not None else _Null()
+    with ctx:
+        for _ in range(steps):
+            per.append(plan.run(T))
+    wall = time.perf_counter() - wall0
+    barrier()
+    return per, wall
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def agg(stats_list):
+    out = {"ms": sum(s.wall_ms for s in stats_list), "kernel_ms": [0.0] * 3, "launches": [0] * 3,
+           "alg": [0] * 3, "h2d": 0, "d2h": 0, "cells": 0, "computed": 0, "exch": 0}
+    for s in stats_list:
+        for i in range(3):
+            out["kernel_ms"][i] += s.kernel_ms[i]
+            out["launches"][i] += s.kernel_launches[i]
+            out["alg"][i] += s.alg_bytes[i]
+        out["h2d"] += s.bytes_h2d
+        out["d2h"] += s.bytes_d2h
+        out["cells"] += s.cell_updates
+        out["computed"] += s.cell_updates_computed
+        out["exch"] += s.bytes_exchange
+    return out
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def cpu_oracle_sample(nx, ny, k, rate, device=None):
+    """Bounded sample of the workload through the CPU oracle: a nx*ny*256 slab (two of c2's
+    128-plane chunks, interior-size trapezoids), one sweep of k steps, BlockQuant rate `rate`."""
+    import oracle
+    import synth
+
+    nz = 256
+    if device is not None:
+        v, p = synth.fields_torch(nx, ny, nz, device=device)
+        v, p = v.cpu().numpy(), p.cpu().numpy()
+    else:
+        v, p = synth.fields(nx, ny, nz)
+    q = rate - 1
+    S = [oracle.encode_planes(a, 1, q) for a in (v, p, p)]
+    ax, ay = nx + 2 * R, ny + 2 * R
+    dt = synth.dt_for()
+
+    def one():
+        Sp, Sc = S[1].copy(), S[2].copy()
+        t0 = time.perf_counter()
+        oracle.pipeline(ax, ay, nz, 2, k, dt, k, 1, q, S[0], Sp, Sc)
+        return time.perf_counter() - t0
+
+    cells = nx * ny * nz * k
+    sample = f"CPU oracle pipeline on a {nx}x{ny}x{nz} slab (2 chunks of 128 planes), 1 sweep of k={k} steps, rate {rate}"
+    return one, cells, sample
+
+
+def threads_used():
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else len(os.sched_getaffinity(0))
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    nx, ny, nzr, nbr, k, T, rate = WORKLOADS[args.workload]
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if dist is None:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    nz = nzr * world
+    nblocks = nbr * world
+    workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps, "
+                f"temporal depth k={k}, BlockQuant rate {rate} bits/value, single working buffer")
+    config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
+              "time_steps_per_step": T, "rate_bits": rate, "mode": "swb", "parallelism": f"z-slabs x{world}",
+              "l2": "inputs larger than L2 (compressed state 6.6 GB/GPU >> 126 MB), no flush needed"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        one, cells, sample = cpu_oracle_sample(nx, ny, k, rate,
+                                               device="cuda" if torch.cuda.is_available() else None)
+        for _ in range(args.warmup):
+            one()
+        secs = sum(one() for _ in range(args.steps))
+        v = cells * args.steps / secs / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 stencil / f32 codec",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
+                                 "sample": sample},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import paper_2204_11315_b200 as oocs
+    from paper_2204_11315_b200 import dist as odist
+
+    dt = float(__import__("synth").dt_for())
+
+    def mk(store, mode="swb", codec="blockquant", profile=False):
+        c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
+                             rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
+                             profile=profile)
+        pl = oocs.Plan(c)
+        if world > 1:
+            pl.set_exchange(odist.nccl_exchange_fn(rank, world))
+        return pl
+
+    peak_gbs, peak_src = measured_peaks()
+    out = {}
+
+    # ---- value: compressed state resident in HBM -------------------------------------------
+    dev = mk("device", profile=True)
+    load_state(dev, nx, ny, nz, local)
+    clocks = ClockSampler(local)
+    per, wall = timed_runs(dev, T, args.steps, args.warmup, barrier, clocks)
+    a = agg(per)
+    dev_ms = allmax(a["ms"])
+    cells_all = allsum(a["cells"])
+    value = cells_all / (dev_ms * 1e-3) / 1e9
+    mem_dev = dev.info.arena_bytes
+    # roofline of the dominant kernel (largest summed launch time)
+    names = ["decode", "step", "encode"]
+    kdom = int(np.argmax(a["kernel_ms"]))
+    launches = max(1, a["launches"][kdom])
+    achieved = a["alg"][kdom] / (a["kernel_ms"][kdom] * 1e-3) / 1e9
+    ncu = ncu_traffic()
+    traffic = None
+    if ncu and names[kdom] in ncu:
+        traffic = ncu[names[kdom]].get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": names[kdom], "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                "frac": achieved / peak_gbs, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": a["alg"][kdom] / launches,
+                "avg_launch_ms": a["kernel_ms"][kdom] / launches,
+                "share_of_step": a["kernel_ms"][kdom] / a["ms"] if a["ms"] else None,
+                "per_kernel": {names[i]: {"ms": a["kernel_ms"][i], "launches": a["launches"][i],
+                                          "GBps": (a["alg"][i] / (a["kernel_ms"][i] * 1e-3) / 1e9)
+                                          if a["kernel_ms"][i] else None} for i in range(3)}}
+    gpu_launches = int(sum(a["launches"]))
+    clk = clocks.summary()
+
+    # ---- e2e: compressed state in pinned host memory, PCIe in the timed region -------------
+    host = mk("host")
+    copy_state(dev, host)
+    dev.close()
+    per_h, wall_h = timed_runs(host, T, args.steps, args.warmup, barrier)
+    ah = agg(per_h)
+    host_ms = allmax(ah["ms"])
+    e2e_value = allsum(ah["cells"]) / (host_ms * 1e-3) / 1e9
+    mem_swb = host.info.arena_bytes
+    pcie_bound = None
+    meas = os.path.join(ROOT, "profiles", "r01_measure_box.json")
+    if os.path.exists(meas):
+        mb = json.load(open(meas))
+        # PCIe roofline of the pipeline: per useful cell-update it must move h2d_pc bytes in and
+        # d2h_pc bytes out; time >= max(in/B_h2d, out/B_d2h, (in+out)/B_duplex) (measured links)
+        h2d_pc = ah["h2d"] / ah["cells"]
+        d2h_pc = ah["d2h"] / ah["cells"]
+        t_pc = max(h2d_pc / mb["h2d_gbs"], d2h_pc / mb["d2h_gbs"], (h2d_pc + d2h_pc) / mb["duplex_total_gbs"])
+        pcie_bound = 1.0 / t_pc
+    e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ah["h2d"] // args.steps,
+           "d2h_bytes_per_step": ah["d2h"] // args.steps, "ms_per_step": host_ms / args.steps,
+           "store": "pinned host (PCIe Gen5)", "pcie_roofline_gcups": pcie_bound,
+           "pcie_frac": (e2e_value / world / pcie_bound) if pcie_bound else None,
+           "h2d_gbs_achieved": ah["h2d"] / (ah["ms"] * 1e-3) / 1e9}
+
+    # ---- paper comparisons: uncompressed pipeline (fig:3ver(a)) and peak memory per mode --------
+    compare = {}
+    if not args.no_compare:
+        mem = {"compress_swb": mem_swb, "device_resident": mem_dev}
+        for mode in ("compress", "dwb"):
+            p = mk("host", mode=mode)
+            mem["compress" if mode == "compress" else "compress_dwb"] = p.info.arena_bytes
+            p.close()
+        base = mk("host", mode="baseline", codec="identity")
+        mem["baseline"] = base.info.arena_bytes
+        load_state(base, nx, ny, nz, local)
+        host.close()
+        per_b, _ = timed_runs(base, T, 1, 1, barrier)
+        ab = agg(per_b)
+        base_ms = allmax(ab["ms"])
+        base_value = allsum(ab["cells"]) / (base_ms * 1e-3) / 1e9
+        base.close()
+        compare = {"uncompressed_baseline_e2e": base_value, "speedup_compressed_vs_uncompressed": e2e_value / base_value,
+                   "paper_speedup_v100": 1.1,
+                   "peak_gpu_mem_gb": {m: v / 1e9 for m, v in mem.items()},
+                   "mem_reduction_swb_vs_baseline": 1 - mem["compress_swb"] / mem["baseline"],
+                   "paper_mem_reduction_v100": 0.33}
+    else:
+        host.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        one, cells, sample = cpu_oracle_sample(nx, ny, k, rate, device=f"cuda:{local}")
+        secs = one()
+        cpu = {"value": cells / secs / 1e9, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
+               "sample": sample, "seconds": secs}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clk,
+                "peak_gpu_mem_gb": mem_swb / 1e9, "value_store": "device-resident compressed state (HBM)",
+                "value_peak_gpu_mem_gb": mem_dev / 1e9, "host_wall_s": wall, "compare": compare,
+                "cell_updates_computed_per_useful": a["computed"] / a["cells"]}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,7 +43,7 @@ cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, i
 cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
                           int codec, int q, int *err, cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
-                        int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
+                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
 
 void set_error(const std::string &msg);
 

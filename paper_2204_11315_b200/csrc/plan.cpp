@@ -107,16 +107,16 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
 // Lowering.  g = global block counter (sweep * nb + local block), lane
 // s(g) = g mod 3 (S:L425 repair of Algorithm 1's never-updated si), working
 // set w(g) = g mod n_ws.  Codec modes follow Algorithm 1 line by line:
-//   iteration g:  [deferred tail of g-1 on lane s(g-1)]
-//                 ENCODE(g-1); RECORD evt_enc(g-1); D2H(g-1); RECORD evt_d2h(g-1)
-//
+//   iteration g:  [lane s(g)] WAIT evt_h2d(g-1); CARRY(g); RECORD evt_carry(g)
+//                      (region sharing: the overlap is copied GPU-side out of the
+//                      previous chunk's half-size buffer before that buffer is reused)
+//                 [deferred tail of g-1 on lane s(g-1)]
+//                 WAIT evt_carry(g); ENCODE(g-1) into hf_buf[s(g-1)]; RECORD evt_enc(g-1);
+//                 D2H(g-1); RECORD evt_d2h(g-1)
 //                 [head of g on lane s(g)]
 //                 WAIT evt_d2h of the previous sweep's chunks whose owned planes this
 //                      H2D reads (cross-sweep RAW on the in-place host store, a10)
-//                 WAIT evt_h2d(g-2)   (staging reuse: carry of g-2 read our buffer)
-//                 H2D(g)             (body only: region sharing P:L87)
-//                 WAIT evt_h2d(g-1); CARRY(g)   (overlap copied on the GPU)
-//                 RECORD evt_h2d(g)
+//                 H2D(g) body into hf_buf[s(g)]; RECORD evt_h2d(g)
 //                 WAIT evt_enc(g - n_ws)         (working-buffer hand-off)
 //                 DECODE(g); RECORD evt_dec(g); STEP(g, 1..k)
 //   drain epilogue after the loop.
@@ -190,8 +190,12 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
         return;
     }
     int64_t pending = -1;
-    auto tail = [&](int64_t p) {
+    // tail of chunk p on its lane; `carry_ev` >= 0: the next chunk's carry copy reads hf_buf[s(p)],
+    // which ENCODE(p) overwrites (one half-size buffer per stream for both directions, P:L146,
+    // P:L153-155), so ENCODE waits for that copy.
+    auto tail = [&](int64_t p, int64_t carry_ev) {
         const int s = lane(p), blk = blk_of(p), t = (int)(p / nb);
+        if (carry_ev >= 0) E.emit(OOCS_OP_WAIT, s, p, blk, t, OOCS_EV_CARRY, carry_ev);
         E.emit(OOCS_OP_ENCODE, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_ENC, p);
         E.emit(OOCS_OP_D2H, s, p, blk, t);
@@ -201,18 +205,19 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
     for (int64_t g = 0; g < G; ++g) {
         const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
         const oocs_block &b = geo.blocks[blk];
+        const bool carry = i > 0 && b.carry_hi > b.carry_lo;
+        if (carry) {  // region sharing: the overlap is copied GPU-side from the previous chunk's buffer
+            E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 1);
+            E.emit(OOCS_OP_CARRY, s, g, blk, t);
+            E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_CARRY, g);
+        }
         if (pending >= 0) {
-            tail(pending);
+            tail(pending, carry ? g : -1);
             pending = -1;
         }
         if (!synced) raw_waits(g, b.body_lo, b.body_hi);
         synced = false;
-        if (g >= 2) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 2);
         E.emit(OOCS_OP_H2D, s, g, blk, t);
-        if (i > 0 && b.carry_hi > b.carry_lo) {
-            E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 1);
-            E.emit(OOCS_OP_CARRY, s, g, blk, t);
-        }
         E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_H2D, g);
         if (g >= geo.n_ws) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_ENC, g - geo.n_ws);
         E.emit(OOCS_OP_DECODE, s, g, blk, t);
@@ -220,13 +225,13 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
         for (int st = 1; st <= geo.k; ++st) E.emit(OOCS_OP_STEP, s, g, blk, t, st);
         pending = g;
         if (multi && i == nb - 1 && t + 1 < sweeps) {
-            tail(pending);
+            tail(pending, -1);
             pending = -1;
             E.emit(OOCS_OP_EXCHANGE, s, g, blk, t);
             synced = true;
         }
     }
-    if (pending >= 0) tail(pending);  // drain epilogue
+    if (pending >= 0) tail(pending, -1);  // drain epilogue
 }
 
 }  // namespace oocs

@@ -39,8 +39,9 @@ struct Plan {
     Arena arena;
     uint64_t arena_bytes = 0, ws_bytes = 0, staging_bytes = 0, store_bytes = 0;
     float *ws[3][N_ARRAYS] = {};     // working sets (fl_buf); [set][array]
-    uint8_t *hf_in[N_LANES] = {};    // compressed in-staging per lane: 3 arrays x max_ext planes
-    uint8_t *hf_out[N_LANES] = {};   // compressed out-staging per lane: 2 arrays x max_own planes
+    uint8_t *hf[N_LANES] = {};       // hf_buf[0:3]: per-lane compressed buffer, used for the
+                                     // chunk coming in (3 arrays x max_ext planes) and, once decoded,
+                                     // for the owned planes going out (2 arrays x max_own planes)
     uint8_t *dstore[2][N_ARRAYS] = {};  // device store (double-buffered pressures; velocity once)
     int cur = 0;
     uint8_t *hstore[N_ARRAYS] = {};  // pinned host store, store_planes x plane_bytes per array
@@ -150,7 +151,7 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
                           cudaStream_t st, oocs_stats *stats) {
     KernelTiming *t = timing_slot(p, 1);
     if (t) CU(cudaEventRecord(t->a, st));
-    CU(launch_step(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, zlo, zhi, p->geo.cfg.dt, st));
+    CU(launch_step(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi, p->geo.cfg.dt, st));
     if (t) CU(cudaEventRecord(t->b, st));
     if (stats) {
         stats->kernel_launches[1]++;
@@ -206,11 +207,10 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
     p->ws_bytes = N_ARRAYS * al(ws_array);
     size_t total = g.n_ws * p->ws_bytes;
     const bool codec_staging = g.host_store && g.cfg.mode != OOCS_MODE_BASELINE;
-    size_t hin = 0, hout = 0;
+    size_t hfb = 0;
     if (codec_staging) {
-        hin = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
-        hout = al((size_t)2 * g.max_own * g.plane_bytes);
-        p->staging_bytes = N_LANES * (hin + hout);
+        hfb = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
+        p->staging_bytes = N_LANES * hfb;
         total += p->staging_bytes;
     }
     const size_t arr_store = (size_t)g.store_planes() * g.plane_bytes;
@@ -240,10 +240,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
     for (int s = 0; s < g.n_ws; ++s)
         for (int a = 0; a < N_ARRAYS; ++a) p->ws[s][a] = (float *)p->arena.take(ws_array);
     if (codec_staging)
-        for (int l = 0; l < N_LANES; ++l) {
-            p->hf_in[l] = (uint8_t *)p->arena.take(hin);
-            p->hf_out[l] = (uint8_t *)p->arena.take(hout);
-        }
+        for (int l = 0; l < N_LANES; ++l) p->hf[l] = (uint8_t *)p->arena.take(hfb);
     if (!g.host_store) {
         p->dstore[0][0] = (uint8_t *)p->arena.take(arr_store);
         p->dstore[1][0] = p->dstore[0][0];
@@ -384,7 +381,7 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
                                       cudaMemcpyHostToDevice, st));
             } else {
                 for (int a = 0; a < N_ARRAYS; ++a)
-                    CU(cudaMemcpyAsync(p->hf_in[s] + ((uint64_t)a * g.max_ext + off) * PB,
+                    CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB,
                                        p->hstore[a] + hoff(p, b.body_lo), nplanes * PB, cudaMemcpyHostToDevice, st));
             }
             if (stats) stats->bytes_h2d += (uint64_t)N_ARRAYS * nplanes * PB;
@@ -406,8 +403,8 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
             } else {
                 const int sp = (int)((o.g - 1) % N_LANES);
                 for (int a = 0; a < N_ARRAYS; ++a)
-                    CU(cudaMemcpyAsync(p->hf_in[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
-                                       p->hf_in[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
+                    CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
+                                       p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
                                        cudaMemcpyDeviceToDevice, st));
                 if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * PB;
             }
@@ -417,7 +414,7 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
             for (int a = 0; a < N_ARRAYS; ++a) {
                 const uint8_t *src;
                 if (g.host_store)
-                    src = p->hf_in[s] + (uint64_t)a * g.max_ext * PB;
+                    src = p->hf[s] + (uint64_t)a * g.max_ext * PB;
                 else
                     src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
                 oocs_status r = k_decode(p, src, wsa(p, w, a), E, st, stats);
@@ -445,7 +442,7 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
             for (int j = 0; j < 2; ++j) {
                 void *dst;
                 if (g.host_store)
-                    dst = p->hf_out[s] + (uint64_t)j * g.max_own * PB;
+                    dst = p->hf[s] + (uint64_t)j * g.max_own * PB;
                 else
                     dst = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
                 oocs_status r = k_encode(p, wsa(p, w, src_arr[j]) + off * g.pstride, dst, W, st, stats);
@@ -464,7 +461,7 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
                                   cudaMemcpyDeviceToHost, st));
             } else {
                 for (int j = 0; j < 2; ++j)
-                    CU(cudaMemcpyAsync(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf_out[s] + (uint64_t)j * g.max_own * PB,
+                    CU(cudaMemcpyAsync(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf[s] + (uint64_t)j * g.max_own * PB,
                                        W * PB, cudaMemcpyDeviceToHost, st));
             }
             if (stats) stats->bytes_d2h += (uint64_t)2 * W * PB;
@@ -770,7 +767,7 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
         set_error("oocs_step: bad geometry or plane range");
         return OOCS_ERR_CONFIG;
     }
-    CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, z_lo, z_hi, dt, (cudaStream_t)stream));
+    CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, planes, z_lo, z_hi, dt, (cudaStream_t)stream));
     return OOCS_OK;
 }
 

@@ -99,6 +99,48 @@ def fields(nx: int, ny: int, nz: int, z_lo: int = 0, z_hi: int | None = None,
     return np.ascontiguousarray(vel, dtype=np.float32), np.ascontiguousarray(p, dtype=np.float32)
 
 
+def fields_torch(nx: int, ny: int, nz: int, z_lo: int = 0, z_hi: int | None = None,
+                 seed: int = SEED, device: str = "cuda"):
+    """Same recipe as fields(kind="layered"), evaluated with torch (float64) on `device` -- for
+    BASELINE-sized grids where numpy would take minutes.  Values agree with fields() to ~1 ulp
+    (different libm); tests that compare against the oracle feed both sides the same arrays."""
+    import torch
+
+    ax, ay, az = nx + 2 * R, ny + 2 * R, nz + 2 * R
+    if z_hi is None:
+        z_hi = az
+    f64 = dict(dtype=torch.float64, device=device)
+    X = torch.arange(0, ax, **f64) - R
+    Y = torch.arange(0, ay, **f64) - R
+    Z = torch.arange(z_lo, z_hi, **f64) - R
+    Xc, Yc, Zc = X.clamp(0, nx - 1), Y.clamp(0, ny - 1), Z.clamp(0, nz - 1)
+    vz = 1.0 + 2.0 * Zc / max(nz - 1, 1)
+    vxy = 0.1 * torch.outer(torch.sin(2 * math.pi * Yc / ny), torch.sin(2 * math.pi * Xc / nx))
+    vel = (vz[:, None, None] + vxy[None]).to(torch.float32)
+    sig = max(2.0, nx / 32.0)
+    p = torch.zeros((len(Z), ay, ax), **f64)
+    for j in range(8):
+        cx = nx * (0.125 + 0.75 * _u01(seed, 3 * j + 0))
+        cy = ny * (0.125 + 0.75 * _u01(seed, 3 * j + 1))
+        cz = nz * (0.125 + 0.75 * _u01(seed, 3 * j + 2))
+        gx = torch.exp(-((X - cx) ** 2) / (2 * sig * sig))
+        gy = torch.exp(-((Y - cy) ** 2) / (2 * sig * sig))
+        gz = torch.exp(-((Z - cz) ** 2) / (2 * sig * sig))
+        p += gz[:, None, None] * torch.outer(gy, gx)[None]
+    for j in range(4):
+        lam = [16.0 + 48.0 * _u01(seed, 100 + 6 * j + a) for a in range(3)]
+        ph = [2 * math.pi * _u01(seed, 103 + 6 * j + a) for a in range(3)]
+        wx = torch.sin(2 * math.pi * X / lam[0] + ph[0])
+        wy = torch.sin(2 * math.pi * Y / lam[1] + ph[1])
+        wz = torch.sin(2 * math.pi * Z / lam[2] + ph[2])
+        p += 0.05 * wz[:, None, None] * torch.outer(wy, wx)[None]
+    inx = ((X >= 0) & (X < nx)).to(torch.float64)
+    iny = ((Y >= 0) & (Y < ny)).to(torch.float64)
+    inz = ((Z >= 0) & (Z < nz)).to(torch.float64)
+    p *= inz[:, None, None] * torch.outer(iny, inx)[None]
+    return vel, p.to(torch.float32)
+
+
 def random_blocks(n_blocks: int, seed: int = 1, special: bool = True) -> np.ndarray:
     """(n_blocks, 64) float32 codec test blocks: mixed scales/offsets, optionally with
     +-0, subnormals, constant blocks and sentinel extremes."""

@@ -48,19 +48,22 @@ def footprint(op, blocks, geo):
                 out.append((("ws", s, a), own_lo - ext_lo, own_hi - ext_lo, False))
                 out.append((("host", a), own_lo, own_hi, True))
         return out
+    # one half-size buffer per lane (hf_buf[s]), in plane units: incoming array a at
+    # [a*ME, a*ME + E), outgoing owned planes of pressure j at [j*MO, j*MO + W)
+    ME, MO = geo["max_ext"], geo["max_own"]
     if kind == "H2D":
         for a in range(3):
             out.append((("host", a), body_lo, body_hi, False))
-            out.append((("hin", s, a), body_lo - ext_lo, ext_hi - ext_lo, True))
+            out.append((("hf", s), a * ME + body_lo - ext_lo, a * ME + ext_hi - ext_lo, True))
     elif kind == "CARRY":
         pb = blocks[op["block"] - 1]
         sp = (g - 1) % 3
         for a in range(3):
-            out.append((("hin", sp, a), c_lo - pb[2], c_hi - pb[2], False))
-            out.append((("hin", s, a), c_lo - ext_lo, c_hi - ext_lo, True))
+            out.append((("hf", sp), a * ME + c_lo - pb[2], a * ME + c_hi - pb[2], False))
+            out.append((("hf", s), a * ME + c_lo - ext_lo, a * ME + c_hi - ext_lo, True))
     elif kind == "DECODE":
         for a in range(3):
-            out.append((("hin", s, a), 0, E, False))
+            out.append((("hf", s), a * ME, a * ME + E, False))
             out.append((("ws", w, a), 0, E, True))
     elif kind == "STEP":
         st = op["arg"]
@@ -74,10 +77,10 @@ def footprint(op, blocks, geo):
         for a in (1, 2):
             out.append((("ws", w, a), own_lo - ext_lo, own_hi - ext_lo, False))
         for j in range(2):
-            out.append((("hout", s, j), 0, own_hi - own_lo, True))
+            out.append((("hf", s), j * MO, j * MO + own_hi - own_lo, True))
     elif kind == "D2H":
         for j in range(2):
-            out.append((("hout", s, j), 0, own_hi - own_lo, False))
+            out.append((("hf", s), j * MO, j * MO + own_hi - own_lo, False))
             out.append((("host", 1 + j), own_lo, own_hi, True))
     return out
 

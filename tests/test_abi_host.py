@@ -75,7 +75,8 @@ def test_encoded_bytes_fixed_rate_law():
 
 def _geo(c, blocks):
     n_ws = {0: 3, 1: 3, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
-    return dict(k=c.tb_depth, n_ws=n_ws, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz)
+    return dict(k=c.tb_depth, n_ws=n_ws, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz,
+                max_ext=max(b[3] - b[2] for b in blocks), max_own=max(b[1] - b[0] for b in blocks))
 
 
 def _check(c, steps):
@@ -138,7 +139,7 @@ def test_deleting_carry_and_cross_sweep_waits_is_detected():
     ops = oocs.oocs_schedule(c, 4)
     blocks = oocs.oocs_plan_table(c)
     geo = _geo(c, blocks)
-    for ev in ("H2D", "D2H"):
+    for ev in ("H2D", "D2H", "CARRY"):
         idx = [i for i, o in enumerate(ops) if o["kind"] == "WAIT" and o["ev"] == ev]
         caught = sum(bool(sc.violations(ops[:i] + ops[i + 1:], blocks, geo, limit=1)) for i in idx)
         assert caught >= 1, ev

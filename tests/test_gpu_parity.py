@@ -252,7 +252,10 @@ def test_lossy_sweep_parity_vs_oracle(n, k, rate):
             tol = step.reshape(az // 4, ay // 4, ax // 4)
             tol = np.repeat(np.repeat(np.repeat(tol, 4, 0), 4, 1), 4, 2)
             amax = np.maximum(np.abs(dg), np.abs(do))
-            assert np.all(np.abs(dg - do) <= tol * 1.01 + 4 * np.spacing(amax.astype(np.float32)) + 1e-30)
+            # + the stencil's own per-step tolerance (1e-6 of max|o|, north star) over the k steps: at
+            # q = 23 a quantisation step is below fp32 stencil rounding
+            stencil_tol = k * 1e-6 * np.max(np.abs(do))
+            assert np.all(np.abs(dg - do) <= tol * 1.01 + 4 * np.spacing(amax.astype(np.float32)) + stencil_tol)
         # continue both sides from the oracle's state (identical inputs each sweep)
         S[1], S[2] = Sp, Sc
         pl.write_raw(1, Sp, 0, az)

@@ -23,10 +23,10 @@ out["h2d_gbs"] = bw(lambda s: d.copy_(h, non_blocking=True), n)
 out["d2h_gbs"] = bw(lambda s: h2.copy_(d, non_blocking=True), n)
 s2 = torch.cuda.Stream()
 def duplex(s):
+    # H2D on s and D2H on s2, both released by the same point of s
+    s2.wait_stream(s)
     d.copy_(h, non_blocking=True)
-    ev = torch.cuda.Event(); 
     with torch.cuda.stream(s2):
-        s2.wait_stream(s)
         h2.copy_(d2, non_blocking=True)
     s.wait_stream(s2)
 out["duplex_total_gbs"] = bw(duplex, 2 * n)

@@ -1,0 +1,19 @@
+"""Representative launches for ncu: one c2 plan with the compressed state in HBM, one warm-up sweep,
+then one profiled sweep (8 chunks x [3 decode + k=4 steps + 2 encode] launches)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2204_11315_b200 as oocs  # noqa: E402
+import synth  # noqa: E402
+
+nx, ny, nz, nb, k, T, rate = bench.WORKLOADS[os.environ.get("WL", "c2")]
+c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, rate_bits=rate,
+                     mode="swb", store="device")
+pl = oocs.Plan(c)
+bench.load_state(pl, nx, ny, nz, 0)
+pl.run(k)
+st = pl.run(k)
+print("sweep ms", st.wall_ms, "launches", list(st.kernel_launches))
