@@ -88,6 +88,10 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
     }
     g->b_lo = (int)((int64_t)c.rank * n / c.world);
     g->b_hi = (int)((int64_t)(c.rank + 1) * n / c.world);
+    // a rank's first chunk has no predecessor on this GPU: its whole extent crosses PCIe
+    // (the halo below it arrives in the ghost planes through the exchange)
+    oocs_block &first = g->blocks[g->b_lo];
+    first.carry_lo = first.carry_hi = first.body_lo = first.ext_lo;
     g->store_lo = std::max<int64_t>(-R, g->blocks[g->b_lo].own_lo - kR);
     g->store_hi = std::min<int64_t>(c.nz + R, g->blocks[g->b_hi - 1].own_hi + kR);
     g->max_ext = g->max_own = 0;
