@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-rank path with several ranks sharing one GPU")
     return ap.parse_args()
 
 
@@ -72,7 +74,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -226,32 +228,6 @@ def main():
     nx, ny, nzr, nbr, k, T, rate = WORKLOADS[args.workload]
     import torch
 
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def allmax(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def allsum(x):
-        if dist is None:
-            return x
-        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        return float(t.item())
-
     nz = nzr * world
     nblocks = nbr * world
     workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps, "
@@ -279,18 +255,51 @@ def main():
         print(json.dumps(line))
         return
 
+    dist = None
+    gloo = args.dist_backend == "gloo"
+    if world > 1:
+        import torch.distributed as dist
+
+        if gloo:
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if gloo else "cuda"
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if dist is None:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
     import paper_2204_11315_b200 as oocs
     from paper_2204_11315_b200 import dist as odist
 
     dt = float(__import__("synth").dt_for())
 
-    def mk(store, mode="swb", codec="blockquant", profile=False):
+    def mk(store, mode="swb", codec="blockquant", profile=False, resident_velocity=False):
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
                              rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
-                             profile=profile)
+                             profile=profile, resident_velocity=resident_velocity)
         pl = oocs.Plan(c)
         if world > 1:
-            pl.set_exchange(odist.nccl_exchange_fn(rank, world))
+            pl.set_exchange((odist.gloo_exchange_fn if gloo else odist.nccl_exchange_fn)(rank, world))
         return pl
 
     peak_gbs, peak_src = measured_peaks()
@@ -314,9 +323,12 @@ def main():
     ncu = ncu_traffic()
     traffic = None
     if ncu and names[kdom] in ncu:
-        traffic = ncu[names[kdom]].get("dram_bytes_per_launch")
+        # DRAM bytes / algorithmic bytes of the profiled launch (ncu --set full), scaled to this run's
+        # average launch
+        traffic = ncu[names[kdom]]["traffic_over_alg"] * a["alg"][kdom] / launches
     roofline = {"bound": "hbm", "kernel": names[kdom], "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                 "frac": achieved / peak_gbs, "traffic": traffic, "peak_source": peak_src,
+                "traffic_source": "profiles/ncu_summary.json (dram__bytes_read+write of one ncu --set full launch)",
                 "alg_bytes_per_launch": a["alg"][kdom] / launches,
                 "avg_launch_ms": a["kernel_ms"][kdom] / launches,
                 "share_of_step": a["kernel_ms"][kdom] / a["ms"] if a["ms"] else None,
@@ -335,7 +347,17 @@ def main():
     host_ms = allmax(ah["ms"])
     e2e_value = allsum(ah["cells"]) / (host_ms * 1e-3) / 1e9
     mem_swb = host.info.arena_bytes
-    pcie_bound = None
+    # variant: compressed velocity kept resident in HBM (OOCS_FLAG_RESIDENT_VELOCITY, SPEC S:L508 flag)
+    hv = mk("host", resident_velocity=True)
+    copy_state(host, hv)
+    per_v, _ = timed_runs(hv, T, args.steps, 1, barrier)
+    av = agg(per_v)
+    hv_ms = allmax(av["ms"])
+    e2e_resident_v = {"value": allsum(av["cells"]) / (hv_ms * 1e-3) / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": av["h2d"] // args.steps, "d2h_bytes_per_step": av["d2h"] // args.steps,
+                      "peak_gpu_mem_gb": hv.info.arena_bytes / 1e9}
+    hv.close()
+    pcie_bound = pcie_bound_5050 = None
     meas = os.path.join(ROOT, "profiles", "r01_measure_box.json")
     if os.path.exists(meas):
         mb = json.load(open(meas))
@@ -345,11 +367,19 @@ def main():
         d2h_pc = ah["d2h"] / ah["cells"]
         t_pc = max(h2d_pc / mb["h2d_gbs"], d2h_pc / mb["d2h_gbs"], (h2d_pc + d2h_pc) / mb["duplex_total_gbs"])
         pcie_bound = 1.0 / t_pc
+        # if concurrent H2D+D2H split the measured duplex rate evenly, the best schedule overlaps the
+        # smaller direction completely and streams the rest alone:
+        lo_, hi_ = min(h2d_pc, d2h_pc), max(h2d_pc, d2h_pc)
+        bhi = mb["h2d_gbs"] if h2d_pc >= d2h_pc else mb["d2h_gbs"]
+        pcie_bound_5050 = 1.0 / (lo_ / (mb["duplex_total_gbs"] / 2) + (hi_ - lo_) / bhi)
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ah["h2d"] // args.steps,
            "d2h_bytes_per_step": ah["d2h"] // args.steps, "ms_per_step": host_ms / args.steps,
            "store": "pinned host (PCIe Gen5)", "pcie_roofline_gcups": pcie_bound,
            "pcie_frac": (e2e_value / world / pcie_bound) if pcie_bound else None,
-           "h2d_gbs_achieved": ah["h2d"] / (ah["ms"] * 1e-3) / 1e9}
+           "pcie_roofline_5050_gcups": pcie_bound_5050 if pcie_bound else None,
+           "pcie_frac_5050": (e2e_value / world / pcie_bound_5050) if pcie_bound else None,
+           "h2d_gbs_achieved": ah["h2d"] / (ah["ms"] * 1e-3) / 1e9,
+           "resident_velocity_variant": e2e_resident_v}
 
     # ---- paper comparisons: uncompressed pipeline (fig:3ver(a)) and peak memory per mode --------
     compare = {}

@@ -19,8 +19,7 @@
  *  - After a CUDA error inside oocs_run/oocs_load/oocs_store the plan is
  *    poisoned: every later call except oocs_destroy returns OOCS_ERR_STATE.
  *  - Pointers are plain host or device pointers as stated per argument; the
- *    library never retains caller pointers beyond the call, except buffers
- *    bound with oocs_plan_bind_arena (caller keeps them alive until destroy).
+ *    library never retains caller pointers beyond the call.
  *  - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
  *    default stream).  No torch type appears in any signature.
  *  - One plan per host thread; plans on different devices may run
@@ -87,6 +86,10 @@ typedef enum {
 } oocs_store_kind;
 
 #define OOCS_FLAG_PROFILE 1u /* time every kernel launch with CUDA events (oocs_stats.kernel_ms) */
+/* Host store only, codec modes: keep this rank's compressed velocity (the read-only dataset,
+ * P:L244) resident in HBM instead of re-sending it every sweep (SPEC S:L508's config flag);
+ * H2D then moves the two pressure arrays only.  Off by default (paper-faithful accounting). */
+#define OOCS_FLAG_RESIDENT_VELOCITY 2u
 
 typedef struct {
     uint32_t struct_size;     /* sizeof(oocs_config): ABI versioning */
@@ -98,6 +101,7 @@ typedef struct {
     int32_t rate_bits;        /* BlockQuant rate r (q = r - 1 code bits); ignored for identity */
     int32_t mode;             /* oocs_mode */
     int32_t region_sharing;   /* 1: reuse the 2kR-plane overlap on the GPU; 0: re-send it */
+    int32_t n_lanes;          /* CUDA streams / half-size buffers of the pipeline: 0 = 3, max 8 */
     int32_t store;            /* oocs_store_kind */
     int32_t device;           /* CUDA device ordinal used by this plan */
     int32_t rank, world;      /* z-slab sharding: this process owns a contiguous run of blocks */
@@ -118,7 +122,7 @@ typedef struct {
     uint64_t staging_bytes;     /* all compressed staging buffers (hf_buf) */
     uint64_t store_bytes;       /* compressed state (host pinned or device) */
     int32_t n_working_sets;     /* 3 (BASELINE/COMPRESS), 1 (SWB), 2 (DWB) */
-    int32_t n_lanes;            /* CUDA streams of the pipeline (3) */
+    int32_t n_lanes;            /* CUDA streams of the pipeline (default 3) */
 } oocs_plan_info;
 
 typedef struct {

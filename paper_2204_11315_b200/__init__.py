@@ -38,6 +38,7 @@ CODEC = {"identity": 0, "blockquant": 1}
 MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
 STORE = {"host": 0, "device": 1}
 FLAG_PROFILE = 1
+FLAG_RESIDENT_VELOCITY = 2
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
 EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY"]
 
@@ -48,7 +49,7 @@ i32, i64, u32, u64, f32, f64, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uin
 class Config(ctypes.Structure):
     _fields_ = [("struct_size", u32), ("nx", i64), ("ny", i64), ("nz", i64), ("dt", f32),
                 ("n_blocks", i32), ("tb_depth", i32), ("codec", i32), ("rate_bits", i32), ("mode", i32),
-                ("region_sharing", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
+                ("region_sharing", i32), ("n_lanes", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
                 ("flags", u32), ("device_capacity", u64)]
 
 
@@ -138,7 +139,7 @@ def _check(st: int, where: str):
 
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
-                device_capacity=0) -> Config:
+                device_capacity=0, n_lanes=0, resident_velocity=False) -> Config:
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -148,9 +149,10 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.rate_bits = rate_bits
     c.mode = MODE[mode] if isinstance(mode, str) else mode
     c.region_sharing = int(region_sharing)
+    c.n_lanes = n_lanes
     c.store = STORE[store] if isinstance(store, str) else store
     c.device, c.rank, c.world = device, rank, world
-    c.flags = FLAG_PROFILE if profile else 0
+    c.flags = (FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
     c.device_capacity = device_capacity
     return c
 

@@ -13,7 +13,7 @@ namespace oocs {
 constexpr int R = OOCS_RADIUS;
 constexpr int XOFF = 32 - R;  // column offset: interior x = R lands on a 128-byte boundary
 constexpr int N_ARRAYS = 3;   // 0 velocity (read-only), 1 pressure t-1, 2 pressure t
-constexpr int N_LANES = 3;    // strm[0:3]
+constexpr int MAX_LANES = 8;  // strm[0:3] in the paper; configurable 2..8
 
 // Geometry derived from a config (pure host; plan.cpp).
 struct Geometry {
@@ -28,6 +28,7 @@ struct Geometry {
     int64_t store_lo, store_hi;      // interior planes held by this rank's store (owned + ghost)
     int64_t max_ext, max_own;        // planes
     int n_ws;               // working sets
+    int lanes;              // CUDA streams = half-size buffers
     bool host_store;
     int64_t a_store_lo() const { return store_lo + R; }  // allocated plane of store index 0
     int64_t store_planes() const { return store_hi - store_lo; }

@@ -38,6 +38,9 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad(err, "bad rank/world");
     if (c->n_blocks % c->world) return bad(err, "world must divide n_blocks (whole chunks per GPU)");
     if (c->device < 0) return bad(err, "bad device ordinal");
+    if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
+        return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
+    if (c->n_lanes != 0 && (c->n_lanes < 2 || c->n_lanes > MAX_LANES)) return bad(err, "n_lanes must be 0 (=3) or 2..8");
     return true;
 }
 
@@ -100,10 +103,11 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
         g->max_own = std::max(g->max_own, g->blocks[i].own_hi - g->blocks[i].own_lo);
     }
     g->host_store = c.store == OOCS_STORE_HOST;
+    g->lanes = c.n_lanes ? c.n_lanes : 3;
     if (!g->host_store)
         g->n_ws = 1;
-    else
-        g->n_ws = c.mode == OOCS_MODE_COMPRESS_SWB ? 1 : c.mode == OOCS_MODE_COMPRESS_DWB ? 2 : 3;
+    else  // SWB: one working buffer; DWB: two; BASELINE / COMPRESS: one per stream (fig:3ver)
+        g->n_ws = c.mode == OOCS_MODE_COMPRESS_SWB ? 1 : c.mode == OOCS_MODE_COMPRESS_DWB ? 2 : g->lanes;
     return OOCS_OK;
 }
 
@@ -159,7 +163,8 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
         }
         return;
     }
-    auto lane = [](int64_t g) { return (int)(g % N_LANES); };
+    const int L = geo.lanes;
+    auto lane = [L](int64_t g) { return (int)(g % L); };
     auto blk_of = [&](int64_t g) { return geo.b_lo + (int)(g % nb); };
     // previous sweep's chunks whose owned planes intersect [lo, hi)
     auto raw_waits = [&](int64_t g, int64_t lo, int64_t hi) {
@@ -182,8 +187,8 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
             else raw_waits(g, b.body_lo, b.body_hi);
             E.emit(OOCS_OP_H2D, s, g, blk, t);
             if (i > 0) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_CARRY, g);
-            if (i + 1 < nb) {
-                if (g >= 2) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_D2H, g - 2);
+            if (i + 1 < nb) {  // the next chunk's working set was last used by chunk g+1-L
+                if (g + 1 >= L) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_D2H, g + 1 - L);
                 E.emit(OOCS_OP_CARRY, s, g + 1, blk + 1, t);
                 E.emit(OOCS_OP_RECORD, s, g + 1, blk + 1, t, OOCS_EV_CARRY, g + 1);
             }

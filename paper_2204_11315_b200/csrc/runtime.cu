@@ -38,20 +38,22 @@ struct Plan {
     Geometry geo;
     Arena arena;
     uint64_t arena_bytes = 0, ws_bytes = 0, staging_bytes = 0, store_bytes = 0;
-    float *ws[3][N_ARRAYS] = {};     // working sets (fl_buf); [set][array]
-    uint8_t *hf[N_LANES] = {};       // hf_buf[0:3]: per-lane compressed buffer, used for the
+    float *ws[MAX_LANES][N_ARRAYS] = {};     // working sets (fl_buf); [set][array]
+    uint8_t *hf[MAX_LANES] = {};       // hf_buf[0:3]: per-lane compressed buffer, used for the
                                      // chunk coming in (3 arrays x max_ext planes) and, once decoded,
                                      // for the owned planes going out (2 arrays x max_own planes)
     uint8_t *dstore[2][N_ARRAYS] = {};  // device store (double-buffered pressures; velocity once)
     int cur = 0;
     uint8_t *hstore[N_ARRAYS] = {};  // pinned host store, store_planes x plane_bytes per array
+    uint8_t *dvel = nullptr;         // OOCS_FLAG_RESIDENT_VELOCITY: compressed velocity kept in HBM
+    bool resident_vel = false;
     uint8_t *xbuf[4] = {};           // exchange buffers: send_lo, send_hi, recv_lo, recv_hi
     uint64_t xbytes = 0;
     int *d_err = nullptr;
-    cudaStream_t lanes[N_LANES] = {};
+    cudaStream_t lanes[MAX_LANES] = {};
     std::vector<cudaEvent_t> ev[5];
     int ev_ring = 0;
-    cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[N_LANES] = {};
+    cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[MAX_LANES] = {};
     oocs_exchange_fn xfn = nullptr;
     void *xuser = nullptr;
     bool poisoned = false;
@@ -210,12 +212,14 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
     size_t hfb = 0;
     if (codec_staging) {
         hfb = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
-        p->staging_bytes = N_LANES * hfb;
+        p->staging_bytes = g.lanes * hfb;
         total += p->staging_bytes;
     }
     const size_t arr_store = (size_t)g.store_planes() * g.plane_bytes;
     p->store_bytes = N_ARRAYS * arr_store;
     if (!g.host_store) total += al(arr_store) * 5;  // v + 2x(p_prev, p_curr)
+    p->resident_vel = (g.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
+    if (p->resident_vel) total += al(arr_store);
     const int64_t kR = (int64_t)g.k * R;
     if (g.cfg.world > 1) {
         p->xbytes = (uint64_t)2 * kR * g.plane_bytes;
@@ -240,13 +244,14 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
     for (int s = 0; s < g.n_ws; ++s)
         for (int a = 0; a < N_ARRAYS; ++a) p->ws[s][a] = (float *)p->arena.take(ws_array);
     if (codec_staging)
-        for (int l = 0; l < N_LANES; ++l) p->hf[l] = (uint8_t *)p->arena.take(hfb);
+        for (int l = 0; l < g.lanes; ++l) p->hf[l] = (uint8_t *)p->arena.take(hfb);
     if (!g.host_store) {
         p->dstore[0][0] = (uint8_t *)p->arena.take(arr_store);
         p->dstore[1][0] = p->dstore[0][0];
         for (int b = 0; b < 2; ++b)
             for (int a = 1; a < N_ARRAYS; ++a) p->dstore[b][a] = (uint8_t *)p->arena.take(arr_store);
     }
+    if (p->resident_vel) p->dvel = (uint8_t *)p->arena.take(arr_store);
     if (g.cfg.world > 1)
         for (int i = 0; i < 4; ++i) p->xbuf[i] = (uint8_t *)p->arena.take(p->xbytes);
     p->d_err = (int *)p->arena.take(sizeof(int));
@@ -273,7 +278,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
             std::memset(p->hstore[a], 0, arr_store);
         }
     }
-    for (int l = 0; l < N_LANES; ++l) {
+    for (int l = 0; l < g.lanes; ++l) {
         if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->lane_done[l], cudaEventDisableTiming) != cudaSuccess) {
             set_error("stream/event creation failed");
@@ -311,7 +316,7 @@ static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
     const int64_t kR = (int64_t)g.k * R;
     const int64_t Zlo = g.blocks[g.b_lo].own_lo, Zhi = g.blocks[g.b_hi - 1].own_hi;
     const bool has_lo = g.cfg.rank > 0, has_hi = g.cfg.rank + 1 < g.cfg.world;
-    for (auto s : p->lanes) CU(cudaStreamSynchronize(s));
+    for (int l = 0; l < g.lanes; ++l) CU(cudaStreamSynchronize(p->lanes[l]));
     cudaStream_t st = p->lanes[0];
     const uint64_t arr = (uint64_t)kR * pb(p);
     // pack: planes [Zlo, Zlo+kR) -> send_lo ; [Zhi-kR, Zhi) -> send_hi ; arrays 1, 2
@@ -365,7 +370,7 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
         const oocs_block &b = blk(o);
         const int64_t E = b.ext_hi - b.ext_lo;
         const int w = (int)(o.g % g.n_ws);
-        const int s = (int)(o.g % N_LANES);
+        const int s = (int)(o.g % g.lanes);
         switch (o.kind) {
         case OOCS_OP_WAIT:
             CU(cudaStreamWaitEvent(st, evt(p, o.arg, o.ev_g), 0));
@@ -380,11 +385,11 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
                     CU(copy_raw_to_ws(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), g, nplanes,
                                       cudaMemcpyHostToDevice, st));
             } else {
-                for (int a = 0; a < N_ARRAYS; ++a)
+                for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
                     CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB,
                                        p->hstore[a] + hoff(p, b.body_lo), nplanes * PB, cudaMemcpyHostToDevice, st));
             }
-            if (stats) stats->bytes_h2d += (uint64_t)N_ARRAYS * nplanes * PB;
+            if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
             break;
         }
         case OOCS_OP_CARRY: {
@@ -401,19 +406,21 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
                                          nplanes * g.ay, cudaMemcpyDeviceToDevice, st));
                 if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
             } else {
-                const int sp = (int)((o.g - 1) % N_LANES);
-                for (int a = 0; a < N_ARRAYS; ++a)
+                const int sp = (int)((o.g - 1) % g.lanes);
+                for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
                     CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
                                        p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
                                        cudaMemcpyDeviceToDevice, st));
-                if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * PB;
+                if (stats) stats->bytes_d2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
             }
             break;
         }
         case OOCS_OP_DECODE: {
             for (int a = 0; a < N_ARRAYS; ++a) {
                 const uint8_t *src;
-                if (g.host_store)
+                if (a == 0 && p->resident_vel)
+                    src = p->dvel + hoff(p, b.ext_lo);
+                else if (g.host_store)
                     src = p->hf[s] + (uint64_t)a * g.max_ext * PB;
                 else
                     src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
@@ -505,10 +512,10 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
     p->timing_used = 0;
     CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->lanes[0]));
     CU(cudaEventRecord(p->t0, p->lanes[0]));
-    for (int l = 1; l < N_LANES; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0, 0));
+    for (int l = 1; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0, 0));
     oocs_status st = execute(p, ops, &stats);
     if (st) return poison(p, st);
-    for (int l = 1; l < N_LANES; ++l) {
+    for (int l = 1; l < g.lanes; ++l) {
         CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
         CU(cudaStreamWaitEvent(p->lanes[0], p->lane_done[l], 0));
     }
@@ -571,6 +578,8 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
             oocs_status r = k_encode(p, ws, stage, n, s, nullptr);
             if (r) return r;
             CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), stage, n * pb(p), cudaMemcpyDeviceToHost, s));
+            if (array == 0 && p->resident_vel)
+                CU(cudaMemcpyAsync(p->dvel + hoff(p, z), stage, n * pb(p), cudaMemcpyDeviceToDevice, s));
         } else {
             for (int b = 0; b < (array == 0 ? 1 : 2); ++b) {
                 oocs_status r = k_encode(p, ws, p->dstore[b][array] + hoff(p, z), n, s, nullptr);
@@ -622,10 +631,12 @@ static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int6
     CU(cudaSetDevice(g.cfg.device));
     const uint64_t off = hoff(p, a_lo - R), n = (uint64_t)(a_hi - a_lo) * pb(p);
     if (g.host_store) {
-        if (write)
+        if (write) {
             std::memcpy(p->hstore[array] + off, host, n);
-        else
+            if (array == 0 && p->resident_vel) CU(cudaMemcpy(p->dvel + off, host, n, cudaMemcpyHostToDevice));
+        } else {
             std::memcpy(host, p->hstore[array] + off, n);
+        }
         return OOCS_OK;
     }
     if (write) {
@@ -692,7 +703,7 @@ oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info) {
     info->staging_bytes = plan->staging_bytes;
     info->store_bytes = plan->store_bytes;
     info->n_working_sets = g.n_ws;
-    info->n_lanes = N_LANES;
+    info->n_lanes = g.lanes;
     return OOCS_OK;
 }
 

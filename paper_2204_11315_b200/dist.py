@@ -52,6 +52,27 @@ def nccl_exchange_fn(rank: int, world: int):
     return fn
 
 
+def gloo_exchange_fn(rank: int, world: int):
+    """Callback for a gloo process group (testing the multi-rank path where NCCL cannot run, e.g. several
+    ranks sharing one GPU): device buffers are staged through host tensors."""
+
+    def fn(sweep, sl, sh, rl, rh, nbytes, stream):
+        torch.cuda.synchronize()
+        t = lambda p: device_bytes(p, nbytes).cpu() if p else None
+        send_lo, send_hi = t(sl), t(sh)
+        recv_lo = torch.empty(nbytes, dtype=torch.uint8) if rl else None
+        recv_hi = torch.empty(nbytes, dtype=torch.uint8) if rh else None
+        halo_exchange(send_lo, send_hi, recv_lo, recv_hi, rank, world)
+        if rl:
+            device_bytes(rl, nbytes).copy_(recv_lo)
+        if rh:
+            device_bytes(rh, nbytes).copy_(recv_hi)
+        torch.cuda.synchronize()
+        return 0
+
+    return fn
+
+
 class LoopbackExchange:
     """In-process exchange between plans of one job that share a GPU (threads, one per rank).
 

@@ -18,7 +18,8 @@ def footprint(op, blocks, geo):
     g = op["g"]
     b = blocks[op["block"]]
     own_lo, own_hi, ext_lo, ext_hi, c_lo, c_hi, body_lo, body_hi = b
-    s = g % 3
+    L = geo.get("lanes", 3)
+    s = g % L
     w = g % n_ws
     E = ext_hi - ext_lo
     out = []
@@ -31,7 +32,7 @@ def footprint(op, blocks, geo):
                 out.append((("ws", s, a), body_lo - ext_lo, ext_hi - ext_lo, True))
         elif kind == "CARRY":  # op.g is the receiving chunk
             pb = blocks[op["block"] - 1]
-            sp = (g - 1) % 3
+            sp = (g - 1) % L
             for a in range(3):
                 out.append((("ws", sp, a), c_lo - pb[2], c_hi - pb[2], False))
                 out.append((("ws", s, a), c_lo - ext_lo, c_hi - ext_lo, True))
@@ -57,7 +58,7 @@ def footprint(op, blocks, geo):
             out.append((("hf", s), a * ME + body_lo - ext_lo, a * ME + ext_hi - ext_lo, True))
     elif kind == "CARRY":
         pb = blocks[op["block"] - 1]
-        sp = (g - 1) % 3
+        sp = (g - 1) % L
         for a in range(3):
             out.append((("hf", sp), a * ME + c_lo - pb[2], a * ME + c_hi - pb[2], False))
             out.append((("hf", s), a * ME + c_lo - ext_lo, a * ME + c_hi - ext_lo, True))
@@ -95,7 +96,7 @@ def happens_before(ops):
         if op["kind"] == "EXCHANGE":
             for j in range(i):
                 succ[j].add(i)
-            last_on_lane = {l: i for l in range(3)}
+            last_on_lane = {l: i for l in range(8)}
             continue
         l = op["lane"]
         if l in last_on_lane:

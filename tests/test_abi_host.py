@@ -74,8 +74,9 @@ def test_encoded_bytes_fixed_rate_law():
 
 
 def _geo(c, blocks):
-    n_ws = {0: 3, 1: 3, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
-    return dict(k=c.tb_depth, n_ws=n_ws, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz,
+    L = c.n_lanes or 3
+    n_ws = {0: L, 1: L, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
+    return dict(k=c.tb_depth, n_ws=n_ws, lanes=L, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz,
                 max_ext=max(b[3] - b[2] for b in blocks), max_own=max(b[1] - b[0] for b in blocks))
 
 
@@ -89,11 +90,12 @@ MODES = [("swb", "blockquant"), ("dwb", "blockquant"), ("compress", "blockquant"
          ("swb", "identity")]
 
 
+@pytest.mark.parametrize("lanes", [0, 2, 4])
 @pytest.mark.parametrize("mode,codec", MODES)
 @pytest.mark.parametrize("n,k,nz", [(1, 1, 16), (2, 1, 32), (3, 2, 48), (4, 2, 64), (5, 3, 80), (8, 1, 64),
                                     (12, 1, 96)])
-def test_schedule_is_race_free(mode, codec, n, k, nz):
-    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec)
+def test_schedule_is_race_free(mode, codec, n, k, nz, lanes):
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec, n_lanes=lanes)
     ops, bad = _check(c, 3 * k)  # three sweeps: exercises the cross-sweep host-store hazards
     assert bad == [], bad[:5]
     # every chunk of every sweep is decoded/computed/encoded exactly once per step

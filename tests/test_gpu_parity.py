@@ -142,9 +142,11 @@ def test_stencil_step_within_1e6(nx, ny, nz):
 
 
 # ----------------------------------------------------------------------------- out-of-core runs
-def make_plan(nx, ny, nz, n, k, codec="blockquant", rate=16, mode="swb", store="host", profile=False):
+def make_plan(nx, ny, nz, n, k, codec="blockquant", rate=16, mode="swb", store="host", profile=False,
+              resident_velocity=False, n_lanes=0):
     c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, codec=codec,
-                         rate_bits=rate, mode=mode, store=store, profile=profile)
+                         rate_bits=rate, mode=mode, store=store, profile=profile,
+                         resident_velocity=resident_velocity, n_lanes=n_lanes)
     return oocs.Plan(c)
 
 
@@ -204,8 +206,12 @@ def test_lossy_modes_are_bitwise_identical(rate):
     vel, p0 = synth.fields(nx, ny, nz)
     az = nz + 2 * R
     outs = []
-    for mode, store in [("compress", "host"), ("swb", "host"), ("dwb", "host"), ("swb", "device")]:
-        pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store)
+    variants = [("compress", "host", False, 0), ("swb", "host", False, 0), ("dwb", "host", False, 0),
+                ("swb", "device", False, 0), ("swb", "host", True, 0), ("swb", "host", False, 4),
+                ("dwb", "host", True, 2)]
+    for mode, store, resident, lanes in variants:
+        pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store, resident_velocity=resident,
+                       n_lanes=lanes)
         load_fields(pl, vel, p0)
         pl.run(6)
         outs.append((pl.read_raw(1, 0, az), pl.read_raw(2, 0, az)))
