@@ -225,12 +225,9 @@ bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int n
             const uint32_t T1 = X((c_lo >> 16) | ((c_hi >> 16) << 16));
             if (st && wi1 >= 0) rec[wi1] = T1;
         }
-        const float bmn = __shfl_sync(0xffffffffu, mn, i), bmx = __shfl_sync(0xffffffffu, mx, i);
-        if (st && lane == 0) {
-            rec[0] = __float_as_uint(bmn);
-            rec[1] = __float_as_uint(bmx);
-        }
     }
+    // block headers straight from the statistics lanes (lane l < 8 holds block l's mn/mx)
+    if (lane < 8 && live) *reinterpret_cast<uint2 *>(rec0 + lane * recw) = make_uint2(__float_as_uint(mn), __float_as_uint(mx));
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1);
 }
 
