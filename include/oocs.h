@@ -202,6 +202,11 @@ oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out);
 oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs_op *ops, int64_t cap,
                           int64_t *n_ops);
 
+/* What oocs_plan_create would allocate for cfg (arena = the device peak, pinned host store, working
+ * sets, staging), without allocating anything: the paper's memory comparison for
+ * configurations larger than this machine.  Errors: OOCS_ERR_CONFIG. */
+oocs_status oocs_plan_estimate(const oocs_config *cfg, oocs_plan_info *info);
+
 /* Compressed bytes of `planes` allocated planes of one array. */
 oocs_status oocs_encoded_bytes(const oocs_config *cfg, int64_t planes, uint64_t *bytes);
 

@@ -21,7 +21,7 @@ import numpy as np
 __all__ = [
     "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
     "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
-    "oocs_plan_query", "oocs_destroy", "oocs_load", "oocs_store", "oocs_store_read_raw",
+    "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_store_read_raw",
     "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
     "oocs_set_exchange", "Plan", "XOFF", "pitch_for",
 ]
@@ -111,6 +111,7 @@ def lib():
             "oocs_encoded_bytes": ([P(Config), i64, P(u64)], i32),
             "oocs_plan_create": ([P(Config), P(vp)], i32),
             "oocs_plan_query": ([vp, P(PlanInfo)], i32),
+            "oocs_plan_estimate": ([P(Config), P(PlanInfo)], i32),
             "oocs_set_exchange": ([vp, EXCHANGE_FN, vp], i32),
             "oocs_destroy": ([vp], i32),
             "oocs_load": ([vp, i32, vp, i64, i64], i32),
@@ -175,6 +176,12 @@ def oocs_schedule(cfg: Config, steps: int):
     _check(lib().oocs_schedule(ctypes.byref(cfg), steps, arr, n.value, ctypes.byref(n)), "oocs_schedule")
     return [dict(kind=OP_KINDS[o.kind], lane=o.lane, g=o.g, block=o.block, sweep=o.sweep, arg=o.arg,
                  ev=(EV_KINDS[o.arg] if o.kind in (6, 7) else None), ev_g=o.ev_g) for o in arr]
+
+
+def oocs_plan_estimate(cfg: Config) -> PlanInfo:
+    info = PlanInfo()
+    _check(lib().oocs_plan_estimate(ctypes.byref(cfg), ctypes.byref(info)), "oocs_plan_estimate")
+    return info
 
 
 def oocs_encoded_bytes(cfg: Config, planes: int) -> int:

@@ -191,6 +191,59 @@ static void free_plan(Plan *p) {
     delete static_cast<oocs_plan *>(p);
 }
 
+// Device arena sizing ("single working buffer" allocator): one pure function shared by
+// oocs_plan_create (which then allocates exactly this) and oocs_plan_estimate (which does not).
+struct Sizes {
+    size_t ws_array = 0, ws_bytes = 0, hfb = 0, staging = 0, arr_store = 0, store_bytes = 0, total = 0;
+    uint64_t xbytes = 0;
+    bool codec_staging = false, resident_vel = false;
+};
+static Sizes compute_sizes(const Geometry &g) {
+    Sizes z;
+    z.ws_array = (size_t)g.max_ext * g.pstride * 4;
+    z.ws_bytes = N_ARRAYS * al(z.ws_array);
+    z.total = g.n_ws * z.ws_bytes;
+    z.codec_staging = g.host_store && g.cfg.mode != OOCS_MODE_BASELINE;
+    if (z.codec_staging) {
+        z.hfb = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
+        z.staging = g.lanes * z.hfb;
+        z.total += z.staging;
+    }
+    z.arr_store = (size_t)g.store_planes() * g.plane_bytes;
+    z.store_bytes = N_ARRAYS * z.arr_store;
+    if (!g.host_store) z.total += al(z.arr_store) * 5;  // v + 2x(p_prev, p_curr)
+    z.resident_vel = (g.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
+    if (z.resident_vel) z.total += al(z.arr_store);
+    if (g.cfg.world > 1) {
+        z.xbytes = (uint64_t)2 * g.k * R * g.plane_bytes;
+        z.total += 4 * al(z.xbytes);
+    }
+    z.total += 256;  // error flag
+    return z;
+}
+
+static void fill_info(const Geometry &g, const Sizes &z, oocs_plan_info *info) {
+    std::memset(info, 0, sizeof(*info));
+    info->ax = g.ax;
+    info->ay = g.ay;
+    info->az = g.az;
+    info->pitch = g.pitch;
+    info->plane_bytes = g.plane_bytes;
+    info->z_lo = g.blocks[g.b_lo].own_lo;
+    info->z_hi = g.blocks[g.b_hi - 1].own_hi;
+    info->store_lo = g.store_lo;
+    info->store_hi = g.store_hi;
+    info->block_lo = g.b_lo;
+    info->block_hi = g.b_hi;
+    info->max_ext_planes = g.max_ext;
+    info->arena_bytes = z.total;
+    info->working_set_bytes = z.ws_bytes;
+    info->staging_bytes = z.staging;
+    info->store_bytes = z.store_bytes;
+    info->n_working_sets = g.n_ws;
+    info->n_lanes = g.lanes;
+}
+
 static oocs_status create(const oocs_config *cfg, Plan **out) {
     *out = nullptr;
     oocs_plan *p = new (std::nothrow) oocs_plan();
@@ -204,28 +257,14 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
     }
     const Geometry &g = p->geo;
     CU(cudaSetDevice(g.cfg.device));
-    // ---- arena sizing ("single working buffer" allocator) ----
-    const size_t ws_array = (size_t)g.max_ext * g.pstride * 4;
-    p->ws_bytes = N_ARRAYS * al(ws_array);
-    size_t total = g.n_ws * p->ws_bytes;
-    const bool codec_staging = g.host_store && g.cfg.mode != OOCS_MODE_BASELINE;
-    size_t hfb = 0;
-    if (codec_staging) {
-        hfb = al((size_t)N_ARRAYS * g.max_ext * g.plane_bytes);
-        p->staging_bytes = g.lanes * hfb;
-        total += p->staging_bytes;
-    }
-    const size_t arr_store = (size_t)g.store_planes() * g.plane_bytes;
-    p->store_bytes = N_ARRAYS * arr_store;
-    if (!g.host_store) total += al(arr_store) * 5;  // v + 2x(p_prev, p_curr)
-    p->resident_vel = (g.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
-    if (p->resident_vel) total += al(arr_store);
-    const int64_t kR = (int64_t)g.k * R;
-    if (g.cfg.world > 1) {
-        p->xbytes = (uint64_t)2 * kR * g.plane_bytes;
-        total += 4 * al(p->xbytes);
-    }
-    total += 256;  // error flag
+    const Sizes z = compute_sizes(g);
+    const size_t ws_array = z.ws_array, hfb = z.hfb, arr_store = z.arr_store, total = z.total;
+    const bool codec_staging = z.codec_staging;
+    p->ws_bytes = z.ws_bytes;
+    p->staging_bytes = z.staging;
+    p->store_bytes = z.store_bytes;
+    p->resident_vel = z.resident_vel;
+    p->xbytes = z.xbytes;
     p->arena_bytes = total;
     if (g.cfg.device_capacity && total > g.cfg.device_capacity) {
         set_error("device arena (" + std::to_string(total) + " B) exceeds device_capacity");
@@ -684,26 +723,20 @@ oocs_status oocs_plan_create(const oocs_config *cfg, oocs_plan **out) {
 oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info) {
     if (oocs_status st = guard(plan)) return st;
     if (!info) return OOCS_ERR_CONFIG;
-    const Geometry &g = plan->geo;
-    std::memset(info, 0, sizeof(*info));
-    info->ax = g.ax;
-    info->ay = g.ay;
-    info->az = g.az;
-    info->pitch = g.pitch;
-    info->plane_bytes = g.plane_bytes;
-    info->z_lo = g.blocks[g.b_lo].own_lo;
-    info->z_hi = g.blocks[g.b_hi - 1].own_hi;
-    info->store_lo = g.store_lo;
-    info->store_hi = g.store_hi;
-    info->block_lo = g.b_lo;
-    info->block_hi = g.b_hi;
-    info->max_ext_planes = g.max_ext;
-    info->arena_bytes = plan->arena_bytes;
-    info->working_set_bytes = plan->ws_bytes;
-    info->staging_bytes = plan->staging_bytes;
-    info->store_bytes = plan->store_bytes;
-    info->n_working_sets = g.n_ws;
-    info->n_lanes = g.lanes;
+    fill_info(plan->geo, compute_sizes(plan->geo), info);
+    return OOCS_OK;
+}
+
+oocs_status oocs_plan_estimate(const oocs_config *cfg, oocs_plan_info *info) {
+    if (!info) return OOCS_ERR_CONFIG;
+    Geometry g;
+    std::string err;
+    oocs_status st = make_geometry(cfg, &g, &err);
+    if (st != OOCS_OK) {
+        set_error(err);
+        return st;
+    }
+    fill_info(g, compute_sizes(g), info);
     return OOCS_OK;
 }
 

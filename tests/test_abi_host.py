@@ -157,3 +157,46 @@ def test_transfer_byte_identities():
         assert ext - body == (n - 1) * 2 * k * oocs.R
         # and the H2D planes of one sweep cover [-R, nz+R) exactly once
         assert body == 96 + 2 * oocs.R
+
+
+def _al(b):
+    return (b + 255) // 256 * 256
+
+
+@pytest.mark.parametrize("rate", [8, 16, 24])
+def test_memory_accounting_paper_units(rate):
+    """baseline = 1 x datasets x 3 streams working buffers; compressed + SWB = 0.5 x 3 x 3 + 1 x
+    datasets.  Our datasets are 3 (the write-only 4th is removed, Q21), so in units of one
+    array's (unpadded) working buffer: baseline 9, COMPRESS 9 + 9r/32, SWB 3 + 9r/32 (= 7.5 at r = 16,
+    the paper's printed figure), DWB 6 + 9r/32."""
+    nx = ny = 100  # ax = 108: working rows padded to 160 floats, compressed planes are not
+    base = dict(nx=nx, ny=ny, nz=256, dt=0.1, n_blocks=4, tb_depth=4, rate_bits=rate)
+    info = {m: oocs.oocs_plan_estimate(cfg(mode=m, codec="identity" if m == "baseline" else "blockquant", **base))
+            for m in ("baseline", "compress", "swb", "dwb")}
+    i = info["swb"]
+    E, ax, ay, pitch = i.max_ext_planes, i.ax, i.ay, i.pitch
+    U_ws = _al(E * ay * pitch * 4)                # one array's working buffer as allocated
+    U_c = E * i.plane_bytes                         # one array's compressed (half-size at r = 16) buffer
+    assert i.plane_bytes * 32 == ax * ay * 4 * rate  # fixed-rate law: r/32 of the fp32 plane
+    assert info["baseline"].arena_bytes == 9 * U_ws + 256
+    assert info["swb"].arena_bytes == 3 * U_ws + 3 * _al(3 * U_c) + 256
+    assert info["dwb"].arena_bytes == 6 * U_ws + 3 * _al(3 * U_c) + 256
+    assert info["compress"].arena_bytes == 9 * U_ws + 3 * _al(3 * U_c) + 256
+    # the same numbers in the paper's units (unpadded working buffer = 1)
+    U = E * ax * ay * 4
+    units = {m: 3 * info[m].n_working_sets + info[m].staging_bytes / U for m in info}
+    assert units["baseline"] == 9
+    assert units["swb"] == pytest.approx(3 + 9 * rate / 32, abs=0.01)
+    if rate == 16:
+        assert units["swb"] == pytest.approx(7.5, abs=0.01)  # "0.5x3x3 + 1x3" (P:L245 prints 7.5)
+        assert 1 - units["swb"] / units["baseline"] == pytest.approx(1 / 6, abs=1e-3)
+
+
+def test_plan_estimate_c5_swb_vs_dwb():
+    # BASELINE configs[4]: 4096x4096x8192, 128 chunks, at 8 B200 -- per-rank arena, SWB vs DWB (no allocation)
+    kw = dict(nx=4096, ny=4096, nz=8192, dt=0.1, n_blocks=128, tb_depth=4, rate_bits=16, world=8)
+    swb = [oocs.oocs_plan_estimate(cfg(mode="swb", rank=r, **kw)) for r in range(8)]
+    dwb = [oocs.oocs_plan_estimate(cfg(mode="dwb", rank=r, **kw)) for r in range(8)]
+    for s, d in zip(swb, dwb):
+        assert d.arena_bytes - s.arena_bytes == s.working_set_bytes  # exactly one more working set
+        assert s.store_bytes > 100e9  # ~104 GB compressed state per rank: truly out of core
