@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
+    ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
+                    help="stream/event schedule of the host-store pipeline (e2e)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank path with several ranks sharing one GPU")
     return ap.parse_args()
@@ -296,7 +298,7 @@ def main():
     def mk(store, mode="swb", codec="blockquant", profile=False, resident_velocity=False):
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
                              rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
-                             profile=profile, resident_velocity=resident_velocity)
+                             profile=profile, resident_velocity=resident_velocity, schedule=args.schedule)
         pl = oocs.Plan(c)
         if world > 1:
             pl.set_exchange((odist.gloo_exchange_fn if gloo else odist.nccl_exchange_fn)(rank, world))
@@ -374,7 +376,7 @@ def main():
         pcie_bound_5050 = 1.0 / (lo_ / (mb["duplex_total_gbs"] / 2) + (hi_ - lo_) / bhi)
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ah["h2d"] // args.steps,
            "d2h_bytes_per_step": ah["d2h"] // args.steps, "ms_per_step": host_ms / args.steps,
-           "store": "pinned host (PCIe Gen5)", "pcie_roofline_gcups": pcie_bound,
+           "store": "pinned host (PCIe Gen5)", "schedule": args.schedule, "pcie_roofline_gcups": pcie_bound,
            "pcie_frac": (e2e_value / world / pcie_bound) if pcie_bound else None,
            "pcie_roofline_5050_gcups": pcie_bound_5050 if pcie_bound else None,
            "pcie_frac_5050": (e2e_value / world / pcie_bound_5050) if pcie_bound else None,

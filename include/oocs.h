@@ -85,6 +85,15 @@ typedef enum {
     OOCS_STORE_DEVICE = 1 /* compressed state resident in HBM (double-buffered); kernels only */
 } oocs_store_kind;
 
+/* How the stream/event schedule is obtained (host store). */
+typedef enum {
+    OOCS_SCHED_ALG1 = 0,     /* Algorithm 1 lowered by hand, with the hazard edges it leaves implicit */
+    OOCS_SCHED_DAG = 1,      /* the paper's general recipe: build the DAG of data dependencies
+                                between chunk operations, Kahn topological sort, record/wait an event for
+                                every cross-stream edge not already implied; one stream per chunk (g mod L) */
+    OOCS_SCHED_DAG_FUNC = 2  /* same DAG, streams by function: H2D + carry / kernels / D2H */
+} oocs_schedule_kind;
+
 #define OOCS_FLAG_PROFILE 1u /* time every kernel launch with CUDA events (oocs_stats.kernel_ms) */
 /* Host store only, codec modes: keep this rank's compressed velocity (the read-only dataset,
  * P:L244) resident in HBM instead of re-sending it every sweep (SPEC S:L508's config flag);
@@ -102,6 +111,7 @@ typedef struct {
     int32_t mode;             /* oocs_mode */
     int32_t region_sharing;   /* 1: reuse the 2kR-plane overlap on the GPU; 0: re-send it */
     int32_t n_lanes;          /* CUDA streams / half-size buffers of the pipeline: 0 = 3, max 8 */
+    int32_t schedule;         /* oocs_schedule_kind */
     int32_t store;            /* oocs_store_kind */
     int32_t device;           /* CUDA device ordinal used by this plan */
     int32_t rank, world;      /* z-slab sharding: this process owns a contiguous run of blocks */
@@ -169,7 +179,8 @@ typedef enum {
     OOCS_EV_DEC = 1,   /* block g decoded */
     OOCS_EV_ENC = 2,   /* block g encoded: working buffer free (Alg. 1 "Record evt[prev_s]") */
     OOCS_EV_D2H = 3,   /* owned planes of block g written back to the host store */
-    OOCS_EV_CARRY = 4  /* BASELINE mode: carry of block g copied into its working buffer */
+    OOCS_EV_CARRY = 4, /* BASELINE mode: carry of block g copied into its working buffer */
+    OOCS_EV_NODE = 5   /* DAG schedules: completion of DAG node ev_g (index in the schedule's node list) */
 } oocs_event_kind;
 
 /* Multi-GPU halo exchange, called by oocs_run on the host after sweep

@@ -37,10 +37,11 @@ STATUS = {0: "OK", 2: "CONFIG", 3: "DEVICE_OOM", 4: "VERIFY", 5: "IO", 6: "DATA"
 CODEC = {"identity": 0, "blockquant": 1}
 MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
 STORE = {"host": 0, "device": 1}
+SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}
 FLAG_PROFILE = 1
 FLAG_RESIDENT_VELOCITY = 2
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
-EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY"]
+EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY", "NODE"]
 
 i32, i64, u32, u64, f32, f64, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
                                     ctypes.c_float, ctypes.c_double, ctypes.c_void_p)
@@ -49,7 +50,7 @@ i32, i64, u32, u64, f32, f64, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uin
 class Config(ctypes.Structure):
     _fields_ = [("struct_size", u32), ("nx", i64), ("ny", i64), ("nz", i64), ("dt", f32),
                 ("n_blocks", i32), ("tb_depth", i32), ("codec", i32), ("rate_bits", i32), ("mode", i32),
-                ("region_sharing", i32), ("n_lanes", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
+                ("region_sharing", i32), ("n_lanes", i32), ("schedule", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
                 ("flags", u32), ("device_capacity", u64)]
 
 
@@ -140,7 +141,7 @@ def _check(st: int, where: str):
 
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
-                device_capacity=0, n_lanes=0, resident_velocity=False) -> Config:
+                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1") -> Config:
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -151,6 +152,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.mode = MODE[mode] if isinstance(mode, str) else mode
     c.region_sharing = int(region_sharing)
     c.n_lanes = n_lanes
+    c.schedule = SCHED[schedule] if isinstance(schedule, str) else schedule
     c.store = STORE[store] if isinstance(store, str) else store
     c.device, c.rank, c.world = device, rank, world
     c.flags = (FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)

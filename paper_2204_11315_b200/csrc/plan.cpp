@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 
 #include "oocs_internal.h"
 
@@ -40,6 +41,7 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->device < 0) return bad(err, "bad device ordinal");
     if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
         return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
+    if (c->schedule < OOCS_SCHED_ALG1 || c->schedule > OOCS_SCHED_DAG_FUNC) return bad(err, "unknown schedule kind");
     if (c->n_lanes != 0 && (c->n_lanes < 2 || c->n_lanes > MAX_LANES)) return bad(err, "n_lanes must be 0 (=3) or 2..8");
     return true;
 }
@@ -147,7 +149,7 @@ struct Emitter {
 };
 }  // namespace
 
-void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
+static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
     ops.clear();
     Emitter E{ops};
     const int nb = geo.nb();
@@ -241,6 +243,227 @@ void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &o
         }
     }
     if (pending >= 0) tail(pending, -1);  // drain epilogue
+}
+
+// ---------------------------------------------------------------------------
+// DAG schedules: "Task graph based methods can be used to schedule the GPU kernels to
+// prevent resource conflicts ... We can schedule the operations by applying topological sorting to
+// the DAG. CUDA events are used to realize fine-grained synchronizations between streams. At the
+// beginning of an arrowed dotted line, we record an event with the stream the line starts from,
+// whereas at the end of the arrowed dotted line, we wait for the event with the stream the arrow is
+// pointed to."
+//   nodes: the chunk operations in the order of the sequential program (Algorithm 1's order);
+//   edges: every pair of nodes touching the same bytes with at least one write (footprints below,
+//          the same model tests/schedule_check.py verifies against);
+//   order: Kahn's algorithm with the program position as priority;
+//   events: a record/wait pair for every cross-stream edge that stream order plus earlier waits do
+//           not already imply (per-node vector clocks over the streams).
+// ---------------------------------------------------------------------------
+namespace {
+struct Acc {
+    int kind, idx, arr;  // kind 0 host store, 1 half-size buffer (arr unused), 2 working buffer
+    int64_t lo, hi;      // plane range
+    bool w;
+};
+
+static void footprint(const Geometry &geo, const oocs_op &o, std::vector<Acc> &f) {
+    f.clear();
+    const int L = geo.lanes;
+    const int64_t g = o.g;
+    const oocs_block &b = geo.blocks[o.block];
+    const int s = (int)(g % L), w = (int)(g % geo.n_ws);
+    const int64_t E = b.ext_hi - b.ext_lo, ME = geo.max_ext, MO = geo.max_own;
+    const bool resv = (geo.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
+    const int a0 = resv ? 1 : 0;
+    const bool base = geo.cfg.mode == OOCS_MODE_BASELINE;
+    auto step_range = [&](int st, int64_t &lo, int64_t &hi) {
+        lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)st * R;
+        hi = (b.ext_hi == geo.nz + R) ? geo.nz : b.ext_hi - (int64_t)st * R;
+    };
+    switch (o.kind) {
+    case OOCS_OP_H2D:
+        for (int a = base ? 0 : a0; a < N_ARRAYS; ++a) {
+            f.push_back({0, 0, a, b.body_lo, b.body_hi, false});
+            if (base)
+                f.push_back({2, w, a, b.body_lo - b.ext_lo, E, true});
+            else
+                f.push_back({1, s, -1, a * ME + b.body_lo - b.ext_lo, a * ME + E, true});
+        }
+        break;
+    case OOCS_OP_CARRY: {
+        const oocs_block &pb = geo.blocks[o.block - 1];
+        const int sp = (int)((g - 1) % L), wp = (int)((g - 1) % geo.n_ws);
+        for (int a = base ? 0 : a0; a < N_ARRAYS; ++a) {
+            if (base) {
+                f.push_back({2, wp, a, b.carry_lo - pb.ext_lo, b.carry_hi - pb.ext_lo, false});
+                f.push_back({2, w, a, b.carry_lo - b.ext_lo, b.carry_hi - b.ext_lo, true});
+            } else {
+                f.push_back({1, sp, -1, a * ME + b.carry_lo - pb.ext_lo, a * ME + b.carry_hi - pb.ext_lo, false});
+                f.push_back({1, s, -1, a * ME + b.carry_lo - b.ext_lo, a * ME + b.carry_hi - b.ext_lo, true});
+            }
+        }
+        break;
+    }
+    case OOCS_OP_DECODE:
+        for (int a = 0; a < N_ARRAYS; ++a) {
+            if (a >= a0) f.push_back({1, s, -1, a * ME, a * ME + E, false});
+            f.push_back({2, w, a, 0, E, true});
+        }
+        break;
+    case OOCS_OP_STEP: {
+        int64_t lo, hi;
+        step_range(o.arg, lo, hi);
+        const int up = (o.arg & 1) ? 1 : 2;
+        f.push_back({2, w, 0, lo - R - b.ext_lo, hi + R - b.ext_lo, false});
+        f.push_back({2, w, 3 - up, lo - R - b.ext_lo, hi + R - b.ext_lo, false});
+        f.push_back({2, w, up, lo - b.ext_lo, hi - b.ext_lo, true});
+        break;
+    }
+    case OOCS_OP_ENCODE:
+        for (int j = 0; j < 2; ++j) {
+            f.push_back({2, w, 1 + j, b.own_lo - b.ext_lo, b.own_hi - b.ext_lo, false});
+            f.push_back({1, s, -1, j * MO, j * MO + b.own_hi - b.own_lo, true});
+        }
+        break;
+    case OOCS_OP_D2H:
+        for (int j = 0; j < 2; ++j) {
+            if (base)
+                f.push_back({2, w, 1 + j, b.own_lo - b.ext_lo, b.own_hi - b.ext_lo, false});
+            else
+                f.push_back({1, s, -1, j * MO, j * MO + b.own_hi - b.own_lo, false});
+            f.push_back({0, 0, 1 + j, b.own_lo, b.own_hi, true});
+        }
+        break;
+    default:
+        break;
+    }
+}
+
+static bool conflict(const std::vector<Acc> &x, const std::vector<Acc> &y) {
+    for (const Acc &a : x)
+        for (const Acc &c : y)
+            if (a.kind == c.kind && a.idx == c.idx && a.arr == c.arr && (a.w || c.w) && a.lo < c.hi && c.lo < a.hi)
+                return true;
+    return false;
+}
+}  // namespace
+
+static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std::vector<oocs_op> &ops) {
+    // 1. nodes = the sequential program (Algorithm 1's operation order, no synchronisation)
+    std::vector<oocs_op> seq;
+    lower_alg1(geo, sweeps, seq);
+    std::vector<oocs_op> nodes;
+    for (const oocs_op &o : seq)
+        if (o.kind != OOCS_OP_WAIT && o.kind != OOCS_OP_RECORD) nodes.push_back(o);
+    const int N = (int)nodes.size();
+    if (by_function)
+        for (oocs_op &o : nodes)
+            if (o.kind != OOCS_OP_EXCHANGE)
+                o.lane = (o.kind == OOCS_OP_H2D || o.kind == OOCS_OP_CARRY) ? 0 : (o.kind == OOCS_OP_D2H ? 2 : 1);
+    // 2. data-dependence edges (u < v in program order); chunks further apart than the window
+    //    share no buffer (ring sizes) and meet on the host store only across one sweep
+    const int L = geo.lanes, nb = geo.nb();
+    const int64_t window = std::max<int64_t>(std::max(L, geo.n_ws), nb) + 2;
+    std::vector<std::vector<Acc>> fp(N);
+    for (int i = 0; i < N; ++i) footprint(geo, nodes[i], fp[i]);
+    std::vector<std::vector<int>> pred(N), succ(N);
+    int last_barrier = -1;
+    for (int v = 0; v < N; ++v) {
+        if (nodes[v].kind == OOCS_OP_EXCHANGE) {
+            for (int u = last_barrier + 1; u < v; ++u) {
+                pred[v].push_back(u);
+                succ[u].push_back(v);
+            }
+            last_barrier = v;
+            continue;
+        }
+        if (last_barrier >= 0 && nodes[last_barrier].kind == OOCS_OP_EXCHANGE) {
+            pred[v].push_back(last_barrier);
+            succ[last_barrier].push_back(v);
+        }
+        for (int u = v - 1; u > last_barrier; --u) {
+            if (nodes[v].g - nodes[u].g > window) break;
+            if (conflict(fp[u], fp[v])) {
+                pred[v].push_back(u);
+                succ[u].push_back(v);
+            }
+        }
+    }
+    // 3. Kahn topological sort, ties broken by program position
+    std::vector<int> indeg(N), order;
+    for (int v = 0; v < N; ++v) indeg[v] = (int)pred[v].size();
+    std::vector<int> ready;  // min-heap on index
+    for (int v = 0; v < N; ++v)
+        if (!indeg[v]) ready.push_back(v);
+    std::make_heap(ready.begin(), ready.end(), std::greater<int>());
+    while (!ready.empty()) {
+        std::pop_heap(ready.begin(), ready.end(), std::greater<int>());
+        const int u = ready.back();
+        ready.pop_back();
+        order.push_back(u);
+        for (int v : succ[u])
+            if (--indeg[v] == 0) {
+                ready.push_back(v);
+                std::push_heap(ready.begin(), ready.end(), std::greater<int>());
+            }
+    }
+    // 4. streams + events: vector clock per node = latest position on every stream known to happen
+    //    before it; a cross-stream edge u->v needs a record/wait unless already covered
+    const int S = MAX_LANES;
+    std::vector<std::vector<int64_t>> vc(N, std::vector<int64_t>(S, -1));
+    std::vector<int64_t> lane_pos(S, -1);
+    std::vector<int> lane_last(S, -1);
+    std::vector<char> recorded(N, 0);
+    std::vector<int64_t> pos(N, -1);
+    std::vector<std::vector<int>> waits(N);
+    for (int v : order) {
+        const oocs_op &o = nodes[v];
+        std::vector<int64_t> c(S, -1);
+        if (o.kind == OOCS_OP_EXCHANGE) {  // executed by the host after draining every stream
+            for (int u : pred[v]) {
+                for (int l = 0; l < S; ++l) c[l] = std::max(c[l], vc[u][l]);
+                c[nodes[u].lane] = std::max(c[nodes[u].lane], pos[u]);
+            }
+            vc[v] = c;
+            for (int l = 0; l < S; ++l) lane_pos[l] = std::max(lane_pos[l], c[l]);
+            continue;
+        }
+        const int l = o.lane;
+        if (lane_last[l] >= 0) {
+            c = vc[lane_last[l]];
+            c[l] = std::max(c[l], pos[lane_last[l]]);
+        }
+        std::vector<int> ps = pred[v];
+        std::sort(ps.begin(), ps.end(), [&](int a, int b2) { return pos[a] > pos[b2]; });
+        for (int u : ps) {
+            if (nodes[u].kind == OOCS_OP_EXCHANGE) continue;
+            const int lu = nodes[u].lane;
+            if (c[lu] >= pos[u]) continue;  // implied by stream order / earlier waits
+            waits[v].push_back(u);
+            recorded[u] = 1;
+            for (int k = 0; k < S; ++k) c[k] = std::max(c[k], vc[u][k]);
+            c[lu] = std::max(c[lu], pos[u]);
+        }
+        pos[v] = ++lane_pos[l];
+        vc[v] = c;
+        lane_last[l] = v;
+    }
+    // 5. emit: waits before the node, the node, its record after it
+    ops.clear();
+    Emitter E{ops};
+    for (int v : order) {
+        const oocs_op &o = nodes[v];
+        for (int u : waits[v]) E.emit(OOCS_OP_WAIT, o.lane, o.g, o.block, o.sweep, OOCS_EV_NODE, u);
+        ops.push_back(o);
+        if (recorded[v]) E.emit(OOCS_OP_RECORD, o.lane, o.g, o.block, o.sweep, OOCS_EV_NODE, v);
+    }
+}
+
+void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
+    if (geo.host_store && geo.cfg.schedule != OOCS_SCHED_ALG1)
+        lower_dag(geo, sweeps, geo.cfg.schedule == OOCS_SCHED_DAG_FUNC, ops);
+    else
+        lower_alg1(geo, sweeps, ops);
 }
 
 }  // namespace oocs

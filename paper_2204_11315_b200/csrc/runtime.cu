@@ -51,7 +51,7 @@ struct Plan {
     uint64_t xbytes = 0;
     int *d_err = nullptr;
     cudaStream_t lanes[MAX_LANES] = {};
-    std::vector<cudaEvent_t> ev[5];
+    std::vector<cudaEvent_t> ev[6];  // per oocs_event_kind, rings indexed by block counter / DAG node
     int ev_ring = 0;
     cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[MAX_LANES] = {};
     oocs_exchange_fn xfn = nullptr;
@@ -88,7 +88,7 @@ static inline uint64_t hoff(const Plan *p, int64_t z) { return (uint64_t)(z - p-
 // device store: same indexing
 static inline float *wsa(Plan *p, int set, int a) { return p->ws[set][a]; }
 
-static cudaEvent_t evt(Plan *p, int kind, int64_t g) { return p->ev[kind][(size_t)(g % p->ev_ring)]; }
+static cudaEvent_t evt(Plan *p, int kind, int64_t g) { return p->ev[kind][(size_t)(g % (int64_t)p->ev[kind].size())]; }
 
 static oocs_status poison(Plan *p, oocs_status st) {
     if (st == OOCS_ERR_CUDA) p->poisoned = true;
@@ -326,8 +326,10 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
         }
     }
     p->ev_ring = g.nb() + 8;
-    for (int k = 0; k < 5; ++k) {
-        p->ev[k].resize(p->ev_ring);
+    // DAG node events: a wait always refers to a node at most `window` chunks back (plan.cpp)
+    const int node_ring = (std::max(std::max(g.lanes, g.n_ws), g.nb()) + 4) * (g.k + 10);
+    for (int k = 0; k < 6; ++k) {
+        p->ev[k].resize(k == OOCS_EV_NODE ? node_ring : p->ev_ring);
         for (auto &e : p->ev[k])
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
                 set_error("event creation failed");

@@ -90,12 +90,13 @@ MODES = [("swb", "blockquant"), ("dwb", "blockquant"), ("compress", "blockquant"
          ("swb", "identity")]
 
 
+@pytest.mark.parametrize("sched", ["alg1", "dag", "dag_func"])
 @pytest.mark.parametrize("lanes", [0, 2, 4])
 @pytest.mark.parametrize("mode,codec", MODES)
 @pytest.mark.parametrize("n,k,nz", [(1, 1, 16), (2, 1, 32), (3, 2, 48), (4, 2, 64), (5, 3, 80), (8, 1, 64),
                                     (12, 1, 96)])
-def test_schedule_is_race_free(mode, codec, n, k, nz, lanes):
-    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec, n_lanes=lanes)
+def test_schedule_is_race_free(mode, codec, n, k, nz, lanes, sched):
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec, n_lanes=lanes, schedule=sched)
     ops, bad = _check(c, 3 * k)  # three sweeps: exercises the cross-sweep host-store hazards
     assert bad == [], bad[:5]
     # every chunk of every sweep is decoded/computed/encoded exactly once per step
@@ -200,3 +201,20 @@ def test_plan_estimate_c5_swb_vs_dwb():
     for s, d in zip(swb, dwb):
         assert d.arena_bytes - s.arena_bytes == s.working_set_bytes  # exactly one more working set
         assert s.store_bytes > 100e9  # ~104 GB compressed state per rank: truly out of core
+
+
+@pytest.mark.parametrize("mode", ["swb", "dwb", "compress"])
+def test_dag_schedule_derives_no_more_waits_than_alg1(mode):
+    # the DAG + Kahn + events recipe reproduces Algorithm 1's operation order and needs at most
+    # as many cross-stream waits as the hand-lowered Algorithm 1 with its hazard repairs
+    c1 = cfg(nz=128, n_blocks=8, tb_depth=2, mode=mode)
+    c2 = cfg(nz=128, n_blocks=8, tb_depth=2, mode=mode, schedule="dag")
+    a, d = oocs.oocs_schedule(c1, 6), oocs.oocs_schedule(c2, 6)
+    core = lambda ops: [(o["kind"], o["lane"], o["g"], o["arg"]) for o in ops if o["kind"] not in ("WAIT", "RECORD")]
+    assert core(a) == core(d)
+    assert sum(o["kind"] == "WAIT" for o in d) <= sum(o["kind"] == "WAIT" for o in a)
+    blocks = oocs.oocs_plan_table(c2)
+    geo = _geo(c2, blocks)
+    idx = [i for i, o in enumerate(d) if o["kind"] == "WAIT"]
+    caught = sum(bool(sc.violations(d[:i] + d[i + 1:], blocks, geo, limit=1)) for i in idx)
+    assert caught >= len(idx) * 3 // 4  # (almost) every derived wait is load-bearing

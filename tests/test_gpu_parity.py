@@ -143,10 +143,10 @@ def test_stencil_step_within_1e6(nx, ny, nz):
 
 # ----------------------------------------------------------------------------- out-of-core runs
 def make_plan(nx, ny, nz, n, k, codec="blockquant", rate=16, mode="swb", store="host", profile=False,
-              resident_velocity=False, n_lanes=0):
+              resident_velocity=False, n_lanes=0, schedule="alg1"):
     c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, codec=codec,
                          rate_bits=rate, mode=mode, store=store, profile=profile,
-                         resident_velocity=resident_velocity, n_lanes=n_lanes)
+                         resident_velocity=resident_velocity, n_lanes=n_lanes, schedule=schedule)
     return oocs.Plan(c)
 
 
@@ -157,7 +157,9 @@ def load_fields(plan, vel, p0):
     plan.load(2, p0, 0, az)
 
 
-IDENTITY_MODES = [("baseline", "host"), ("compress", "host"), ("swb", "host"), ("dwb", "host"), ("swb", "device")]
+IDENTITY_MODES = [("baseline", "host", "alg1"), ("compress", "host", "alg1"), ("swb", "host", "alg1"),
+                  ("dwb", "host", "alg1"), ("swb", "device", "alg1"), ("baseline", "host", "dag_func"),
+                  ("swb", "host", "dag")]
 
 
 @pytest.mark.parametrize("n,k", [(4, 2), (3, 1), (2, 3), (1, 2)])
@@ -167,8 +169,8 @@ def test_identity_pipeline_bitwise_all_modes_and_vs_oracle(n, k):
     az = nz + 2 * R
     T = 2 * k
     results = []
-    for mode, store in IDENTITY_MODES:
-        pl = make_plan(nx, ny, nz, n, k, codec="identity", mode=mode, store=store)
+    for mode, store, sched in IDENTITY_MODES:
+        pl = make_plan(nx, ny, nz, n, k, codec="identity", mode=mode, store=store, schedule=sched)
         load_fields(pl, vel, p0)
         st = pl.run(T)
         results.append((pl.store(1, 0, az), pl.store(2, 0, az)))
@@ -206,12 +208,14 @@ def test_lossy_modes_are_bitwise_identical(rate):
     vel, p0 = synth.fields(nx, ny, nz)
     az = nz + 2 * R
     outs = []
-    variants = [("compress", "host", False, 0), ("swb", "host", False, 0), ("dwb", "host", False, 0),
-                ("swb", "device", False, 0), ("swb", "host", True, 0), ("swb", "host", False, 4),
-                ("dwb", "host", True, 2)]
-    for mode, store, resident, lanes in variants:
+    variants = [("compress", "host", False, 0, "alg1"), ("swb", "host", False, 0, "alg1"),
+                ("dwb", "host", False, 0, "alg1"), ("swb", "device", False, 0, "alg1"),
+                ("swb", "host", True, 0, "alg1"), ("swb", "host", False, 4, "alg1"), ("dwb", "host", True, 2, "alg1"),
+                ("swb", "host", False, 0, "dag"), ("swb", "host", False, 0, "dag_func"),
+                ("compress", "host", True, 4, "dag_func")]
+    for mode, store, resident, lanes, sched in variants:
         pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store, resident_velocity=resident,
-                       n_lanes=lanes)
+                       n_lanes=lanes, schedule=sched)
         load_fields(pl, vel, p0)
         pl.run(6)
         outs.append((pl.read_raw(1, 0, az), pl.read_raw(2, 0, az)))
