@@ -23,6 +23,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 R = 4  # stencil radius (P:L190 HALO=4, P:L212 25-point)
 CODEC_IDENTITY = 0
 CODEC_BLOCKQUANT = 1
+CODEC_ZFP = 2  # the codec parameter is the rate (bits/value) for ZFP, q = rate - 1 for BlockQuant
 
 
 def build(force: bool = False) -> str:
@@ -59,6 +60,17 @@ def lib():
         L.oracle_plan.restype = i32
         L.oracle_pipeline.argtypes = [i64, i64, i64, i64, i64, f32, i64, i32, i32, vp, vp, vp]
         L.oracle_pipeline.restype = i32
+        L.oracle_zfp_encode_block.argtypes = [vp, i32, vp]
+        L.oracle_zfp_encode_block.restype = i32
+        L.oracle_zfp_decode_block.argtypes = [vp, i32, vp]
+        L.oracle_zfp_fwd_lift.argtypes = [vp, i32]
+        L.oracle_zfp_inv_lift.argtypes = [vp, i32]
+        L.oracle_zfp_fwd_xform.argtypes = [vp]
+        L.oracle_zfp_inv_xform.argtypes = [vp]
+        L.oracle_zfp_int2uint.argtypes = [ctypes.c_int32]
+        L.oracle_zfp_int2uint.restype = ctypes.c_uint32
+        L.oracle_zfp_uint2int.argtypes = [ctypes.c_uint32]
+        L.oracle_zfp_uint2int.restype = ctypes.c_int32
         _lib = L
     return _lib
 
@@ -147,3 +159,40 @@ def pipeline(ax, ay, nz, n, k, dt, steps, codec, q, S_vel, S_prev, S_curr):
     if rc:
         raise OracleError(rc)
     return S_prev, S_curr
+
+
+# ---- ZFP (NEXT-1) ------------------------------------------------------------
+def zfp_encode_block(x, rate: int) -> bytes:
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(64)
+    rec = np.zeros(rate, dtype=np.uint64)
+    rc = lib().oracle_zfp_encode_block(_p(x), rate, _p(rec))
+    if rc:
+        raise OracleError(rc)
+    return rec.tobytes()
+
+
+def zfp_decode_block(rec: bytes, rate: int) -> np.ndarray:
+    r = np.frombuffer(rec, dtype=np.uint64).copy()
+    x = np.zeros(64, dtype=np.float32)
+    lib().oracle_zfp_decode_block(_p(r), rate, _p(x))
+    return x
+
+
+def zfp_lift(v, inverse=False):
+    a = np.ascontiguousarray(v, dtype=np.int32).copy()
+    (lib().oracle_zfp_inv_lift if inverse else lib().oracle_zfp_fwd_lift)(_p(a), 1)
+    return a
+
+
+def zfp_xform(b, inverse=False):
+    a = np.ascontiguousarray(b, dtype=np.int32).reshape(64).copy()
+    (lib().oracle_zfp_inv_xform if inverse else lib().oracle_zfp_fwd_xform)(_p(a))
+    return a
+
+
+def zfp_int2uint(x: int) -> int:
+    return int(lib().oracle_zfp_int2uint(x))
+
+
+def zfp_uint2int(u: int) -> int:
+    return int(lib().oracle_zfp_uint2int(u))

@@ -38,8 +38,13 @@
  * contraction (built with -ffp-contract=off), no flush-to-zero.  fmaf() is
  * the C99 correctly-rounded fused multiply-add.
  *
+ *   oracle_zfp_*             NEXT-1: the ZFP fixed-rate codec (cuZFP's algorithm,
+ *                            P:L116), codec 2 in the array-level calls
+ *                            and the pipeline (the codec argument `q` is the rate)
+ *
  * Everything here is pinned; see DESIGN.md §5 for the pin list.  Nothing is
- * "parity unpinned" except what DESIGN.md names.
+ * "parity unpinned" except what DESIGN.md names (ZFP bitstream compatibility
+ * with the zfp library itself).
  */
 #include <math.h>
 #include <stdint.h>
@@ -203,10 +208,14 @@ void oracle_bq_decode_block(const uint8_t *rec, int q, float *x) {
     for (int j = 0; j < 64; ++j) x[j] = fmaf((float)code[j] + 0.5f, step, mn);
 }
 
+int oracle_zfp_encode_planes(int64_t ax, int64_t ay, int64_t planes, const float *src, int rate, uint8_t *dst);
+void oracle_zfp_decode_planes(int64_t ax, int64_t ay, int64_t planes, const uint8_t *src, int rate, float *dst);
+
 /* Bytes of one compressed plane-slab-row: an allocated xy plane of ax*ay
  * values costs ax*ay*rate_bits/8 bytes; identity (codec 0) costs 4 B/value. */
 int64_t oracle_plane_bytes(int64_t ax, int64_t ay, int codec, int q) {
     if (codec == 0) return ax * ay * 4;
+    if (codec == 2) return (ax / 4) * (ay / 4) * 8 * q / 4; /* ZFP: q is the rate (bits/value) */
     return (ax / 4) * (ay / 4) * 8 * (q + 1) / 4;
 }
 
@@ -222,6 +231,7 @@ int oracle_encode_planes(int64_t ax, int64_t ay, int64_t planes, const float *sr
         memcpy(dst, src, (size_t)(ax * ay * planes) * 4);
         return ORACLE_OK;
     }
+    if (codec == 2) return oracle_zfp_encode_planes(ax, ay, planes, src, q, dst);
     if (ax % 4 || ay % 4 || planes % 4) return ORACLE_ERR_CONFIG;
     const int64_t nbx = ax / 4, nby = ay / 4, nbz = planes / 4;
     const int64_t rec_bytes = 8 * (q + 1);
@@ -247,6 +257,10 @@ void oracle_decode_planes(int64_t ax, int64_t ay, int64_t planes, const uint8_t 
                           int codec, int q, float *dst) {
     if (codec == 0) {
         memcpy(dst, src, (size_t)(ax * ay * planes) * 4);
+        return;
+    }
+    if (codec == 2) {
+        oracle_zfp_decode_planes(ax, ay, planes, src, q, dst);
         return;
     }
     const int64_t nbx = ax / 4, nby = ay / 4, nbz = planes / 4;
@@ -383,4 +397,254 @@ int oracle_pipeline(int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k, fl
     free(N_curr);
     free(plan);
     return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* ZFP fixed-rate codec (NEXT-1): the algorithm of zfp 0.5.5 as used by  */
+/* cuZFP, 3-D float blocks, written out step by step:  */
+/*   1. block-floating-point: common exponent emax of the 64 values,     */
+/*      values scaled to 30-bit signed integers (truncation);            */
+/*   2. decorrelating transform: integer lifting along x, then y, then z;*/
+/*   3. reorder by total sequency, map to negabinary;                    */
+/*   4. embedded coding of bit planes, MSB first, with group testing,    */
+/*      truncated at maxbits = 64 * rate bits (fixed rate).              */
+/* Record = maxbits bits, written LSB-first into 64-bit words.           */
+/* Bitstream compatibility with the zfp library itself is parity         */
+/* unpinned (no zfp in this environment); the pins are the transform's   */
+/* documented matrices, the embedded-prefix property, exact cases and   */
+/* error behaviour (tests/test_oracle_zfp.py).                          */
+/* ------------------------------------------------------------------ */
+
+#define ZFP_EBITS 8
+#define ZFP_EBIAS 127
+#define ZFP_NBMASK 0xaaaaaaaau
+
+typedef struct {
+    uint64_t *w; /* words */
+    int64_t pos; /* bit position */
+} oracle_bits;
+
+static void zb_put(oracle_bits *s, uint64_t bit) {
+    if (bit & 1u) s->w[s->pos >> 6] |= (uint64_t)1 << (s->pos & 63);
+    s->pos++;
+}
+static uint64_t zb_get(oracle_bits *s) {
+    uint64_t b = (s->w[s->pos >> 6] >> (s->pos & 63)) & 1u;
+    s->pos++;
+    return b;
+}
+
+/* sequency order of the 64 coefficients of a 4x4x4 block: coefficient (i, j, k) of the
+ * transform sits at i + 4j + 16k; listed by non-decreasing total sequency i + j + k, in zfp's
+ * order (perm_3) */
+#define ZI(i, j, k) ((i) + 4 * (j) + 16 * (k))
+const unsigned char zfp_perm3[64] = {
+    ZI(0,0,0), ZI(1,0,0), ZI(0,1,0), ZI(0,0,1), ZI(0,1,1), ZI(1,0,1),
+    ZI(1,1,0), ZI(2,0,0), ZI(0,2,0), ZI(0,0,2), ZI(1,1,1), ZI(2,1,0),
+    ZI(2,0,1), ZI(0,2,1), ZI(1,2,0), ZI(1,0,2), ZI(0,1,2), ZI(3,0,0),
+    ZI(0,3,0), ZI(0,0,3), ZI(2,1,1), ZI(1,2,1), ZI(1,1,2), ZI(0,2,2),
+    ZI(2,0,2), ZI(2,2,0), ZI(3,1,0), ZI(3,0,1), ZI(0,3,1), ZI(1,3,0),
+    ZI(1,0,3), ZI(0,1,3), ZI(1,2,2), ZI(2,1,2), ZI(2,2,1), ZI(3,1,1),
+    ZI(1,3,1), ZI(1,1,3), ZI(3,2,0), ZI(3,0,2), ZI(0,3,2), ZI(2,3,0),
+    ZI(2,0,3), ZI(0,2,3), ZI(2,2,2), ZI(3,2,1), ZI(3,1,2), ZI(1,3,2),
+    ZI(2,3,1), ZI(2,1,3), ZI(1,2,3), ZI(0,3,3), ZI(3,0,3), ZI(3,3,0),
+    ZI(3,2,2), ZI(2,3,2), ZI(2,2,3), ZI(1,3,3), ZI(3,1,3), ZI(3,3,1),
+    ZI(2,3,3), ZI(3,2,3), ZI(3,3,2), ZI(3,3,3),
+};
+#undef ZI
+
+/* forward lifting of 4 values p[0], p[s], p[2s], p[3s] (zfp fwd_lift):
+ *          ( 4  4  4  4)
+ *   1/16 * ( 5  1 -1 -5)
+ *          (-4  4  4 -4)
+ *          (-2  6 -6  2)   (exact when no shift drops bits) */
+void oracle_zfp_fwd_lift(int32_t *p, int s) {
+    int32_t x = p[0], y = p[s], z = p[2 * s], w = p[3 * s];
+    x += w; x >>= 1; w -= x;
+    z += y; z >>= 1; y -= z;
+    x += z; x >>= 1; z -= x;
+    w += y; w >>= 1; y -= w;
+    w += y >> 1; y -= w >> 1;
+    p[0] = x; p[s] = y; p[2 * s] = z; p[3 * s] = w;
+}
+
+/* inverse lifting (zfp inv_lift):
+ *         ( 4  6 -4 -1)
+ *   1/4 * ( 4  2  4  5)
+ *         ( 4 -2  4 -5)
+ *         ( 4 -6 -4  1) */
+void oracle_zfp_inv_lift(int32_t *p, int s) {
+    int32_t x = p[0], y = p[s], z = p[2 * s], w = p[3 * s];
+    y += w >> 1; w -= y >> 1;
+    y += w; w <<= 1; w -= y;
+    z += x; x <<= 1; x -= z;
+    y += z; z <<= 1; z -= y;
+    w += x; x <<= 1; x -= w;
+    p[0] = x; p[s] = y; p[2 * s] = z; p[3 * s] = w;
+}
+
+void oracle_zfp_fwd_xform(int32_t *b) {
+    for (int z = 0; z < 4; z++)
+        for (int y = 0; y < 4; y++) oracle_zfp_fwd_lift(b + 4 * y + 16 * z, 1);
+    for (int x = 0; x < 4; x++)
+        for (int z = 0; z < 4; z++) oracle_zfp_fwd_lift(b + 16 * z + x, 4);
+    for (int y = 0; y < 4; y++)
+        for (int x = 0; x < 4; x++) oracle_zfp_fwd_lift(b + x + 4 * y, 16);
+}
+
+void oracle_zfp_inv_xform(int32_t *b) {
+    for (int y = 0; y < 4; y++)
+        for (int x = 0; x < 4; x++) oracle_zfp_inv_lift(b + x + 4 * y, 16);
+    for (int x = 0; x < 4; x++)
+        for (int z = 0; z < 4; z++) oracle_zfp_inv_lift(b + 16 * z + x, 4);
+    for (int z = 0; z < 4; z++)
+        for (int y = 0; y < 4; y++) oracle_zfp_inv_lift(b + 4 * y + 16 * z, 1);
+}
+
+uint32_t oracle_zfp_int2uint(int32_t x) { return ((uint32_t)x + ZFP_NBMASK) ^ ZFP_NBMASK; }
+int32_t oracle_zfp_uint2int(uint32_t x) { return (int32_t)((x ^ ZFP_NBMASK) - ZFP_NBMASK); }
+
+/* exponent of x >= 0 as frexp gives it, clamped for denormals; -EBIAS for 0 */
+static int zfp_exponent(float x) {
+    if (x > 0) {
+        int e;
+        frexpf(x, &e);
+        return e > 1 - ZFP_EBIAS ? e : 1 - ZFP_EBIAS;
+    }
+    return -ZFP_EBIAS;
+}
+
+/* encode one block of 64 floats (j = xi + 4 yi + 16 zi) into maxbits = 64*rate bits
+ * (the record must be zeroed by the caller).  Returns ORACLE_ERR_DATA on NaN/Inf. */
+int oracle_zfp_encode_block(const float *x, int rate, uint64_t *rec) {
+    const int maxbits = 64 * rate;
+    float amax = 0;
+    for (int j = 0; j < 64; ++j) {
+        if (!isfinite(x[j])) return ORACLE_ERR_DATA;
+        if (fabsf(x[j]) > amax) amax = fabsf(x[j]);
+    }
+    oracle_bits s = {rec, 0};
+    const int emax = zfp_exponent(amax);
+    const unsigned e = (unsigned)(emax + ZFP_EBIAS); /* fixed-rate: precision is never 0 for floats */
+    if (!e) { /* all zeros: a single 0 bit, rest padding */
+        zb_put(&s, 0);
+        return ORACLE_OK;
+    }
+    /* 1. header: 2e+1 in 1 + EBITS bits (LSB = "nonzero block") */
+    const uint64_t head = 2 * (uint64_t)e + 1;
+    for (int i = 0; i < 1 + ZFP_EBITS; ++i) zb_put(&s, head >> i);
+    /* block-floating-point: integer = (int)(x * 2^(30 - emax)), truncation toward zero */
+    /* (zfp forms 2^(30-emax) in float, which overflows for emax < -97; in double the product is
+     * exact and identical wherever zfp's is defined) */
+    int32_t ib[64];
+    const double scale = ldexp(1.0, 30 - emax);
+    for (int j = 0; j < 64; ++j) ib[j] = (int32_t)(scale * (double)x[j]);
+    /* 2. decorrelating transform */
+    oracle_zfp_fwd_xform(ib);
+    /* 3. sequency order + negabinary */
+    uint32_t ub[64];
+    for (int i = 0; i < 64; ++i) ub[i] = oracle_zfp_int2uint(ib[zfp_perm3[i]]);
+    /* 4. embedded bit-plane coding with group tests (zfp encode_ints, kmin = 0) */
+    unsigned bits = (unsigned)(maxbits - 1 - ZFP_EBITS);
+    unsigned n = 0;
+    for (int k = 32; bits && k-- > 0;) {
+        uint64_t plane = 0;
+        for (int i = 0; i < 64; ++i) plane += (uint64_t)((ub[i] >> k) & 1u) << i;
+        /* the first n coefficients are already significant: their bits verbatim */
+        unsigned m = n < bits ? n : bits;
+        bits -= m;
+        for (unsigned i = 0; i < m; ++i) zb_put(&s, plane >> i);
+        plane = m == 64 ? 0 : plane >> m;
+        /* unary run-length code of the remainder: group test, then the next 1 */
+        for (; n < 64 && bits; plane >>= 1, n++) {
+            bits--;
+            zb_put(&s, plane != 0);
+            if (!plane) break;
+            for (; n < 63 && bits; plane >>= 1, n++) {
+                bits--;
+                zb_put(&s, plane & 1u);
+                if (plane & 1u) break;
+            }
+        }
+    }
+    return ORACLE_OK;
+}
+
+void oracle_zfp_decode_block(const uint64_t *rec, int rate, float *x) {
+    const int maxbits = 64 * rate;
+    oracle_bits s = {(uint64_t *)rec, 0};
+    if (!zb_get(&s)) {
+        for (int j = 0; j < 64; ++j) x[j] = 0.0f;
+        return;
+    }
+    unsigned e = 0;
+    for (int i = 0; i < ZFP_EBITS; ++i) e |= (unsigned)zb_get(&s) << i;
+    const int emax = (int)e - ZFP_EBIAS;
+    uint32_t ub[64] = {0};
+    unsigned bits = (unsigned)(maxbits - 1 - ZFP_EBITS);
+    unsigned n = 0;
+    for (int k = 32; bits && k-- > 0;) {
+        unsigned m = n < bits ? n : bits;
+        bits -= m;
+        uint64_t plane = 0;
+        for (unsigned i = 0; i < m; ++i) plane |= zb_get(&s) << i;
+        for (; n < 64 && bits; ) {
+            bits--;
+            if (!zb_get(&s)) break;
+            for (; n < 63 && bits; n++) {
+                bits--;
+                if (zb_get(&s)) break;
+            }
+            plane += (uint64_t)1 << n;
+            n++;
+        }
+        for (int i = 0; i < 64; ++i) ub[i] += (uint32_t)((plane >> i) & 1u) << k;
+    }
+    int32_t ib[64];
+    for (int i = 0; i < 64; ++i) ib[zfp_perm3[i]] = oracle_zfp_uint2int(ub[i]);
+    oracle_zfp_inv_xform(ib);
+    /* inverse block-floating-point: (float)int * 2^(emax-30) (zfp inv_cast; in double, exact) */
+    const double scale = ldexp(1.0, emax - 30);
+    for (int j = 0; j < 64; ++j) x[j] = (float)((double)(float)ib[j] * scale);
+}
+
+/* Array-level ZFP over whole 4-plane slabs, same slab-major block order as BlockQuant; each block
+ * record is 64*rate bits = 8*rate bytes. */
+int oracle_zfp_encode_planes(int64_t ax, int64_t ay, int64_t planes, const float *src, int rate, uint8_t *dst) {
+    if (ax % 4 || ay % 4 || planes % 4 || rate < 1 || rate > 32) return ORACLE_ERR_CONFIG;
+    const int64_t nbx = ax / 4, nby = ay / 4, nbz = planes / 4;
+    const int64_t rec_bytes = 8 * rate;
+    int err = ORACLE_OK;
+#pragma omp parallel for schedule(static) reduction(| : err)
+    for (int64_t bz = 0; bz < nbz; ++bz) {
+        float blk[64];
+        for (int64_t by = 0; by < nby; ++by)
+            for (int64_t bx = 0; bx < nbx; ++bx) {
+                for (int zi = 0; zi < 4; ++zi)
+                    for (int yi = 0; yi < 4; ++yi)
+                        for (int xi = 0; xi < 4; ++xi)
+                            blk[xi + 4 * yi + 16 * zi] = src[((4 * bz + zi) * ay + 4 * by + yi) * ax + 4 * bx + xi];
+                uint64_t *rec = (uint64_t *)(dst + ((bz * nby + by) * nbx + bx) * rec_bytes);
+                memset(rec, 0, (size_t)rec_bytes);
+                err |= oracle_zfp_encode_block(blk, rate, rec);
+            }
+    }
+    return err ? ORACLE_ERR_DATA : ORACLE_OK;
+}
+
+void oracle_zfp_decode_planes(int64_t ax, int64_t ay, int64_t planes, const uint8_t *src, int rate, float *dst) {
+    const int64_t nbx = ax / 4, nby = ay / 4, nbz = planes / 4;
+    const int64_t rec_bytes = 8 * rate;
+#pragma omp parallel for schedule(static)
+    for (int64_t bz = 0; bz < nbz; ++bz) {
+        float blk[64];
+        for (int64_t by = 0; by < nby; ++by)
+            for (int64_t bx = 0; bx < nbx; ++bx) {
+                oracle_zfp_decode_block((const uint64_t *)(src + ((bz * nby + by) * nbx + bx) * rec_bytes), rate, blk);
+                for (int zi = 0; zi < 4; ++zi)
+                    for (int yi = 0; yi < 4; ++yi)
+                        for (int xi = 0; xi < 4; ++xi)
+                            dst[((4 * bz + zi) * ay + 4 * by + yi) * ax + 4 * bx + xi] = blk[xi + 4 * yi + 16 * zi];
+            }
+    }
 }
