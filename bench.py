@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
+    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp"],
+                    help="fixed-rate codec of the compressed state (ZFP = NEXT-1)")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
                     help="stream/event schedule of the host-store pipeline (e2e)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -233,9 +235,11 @@ def main():
     nz = nzr * world
     nblocks = nbr * world
     workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps, "
-                f"temporal depth k={k}, BlockQuant rate {rate} bits/value, single working buffer")
+                f"temporal depth k={k}, {'ZFP' if args.codec == 'zfp' else 'BlockQuant'} rate {rate} bits/value, "
+                f"single working buffer")
     config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
-              "time_steps_per_step": T, "rate_bits": rate, "mode": "swb", "parallelism": f"z-slabs x{world}",
+              "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
+              "parallelism": f"z-slabs x{world}",
               "l2": "inputs larger than L2 (compressed state 6.6 GB/GPU >> 126 MB), no flush needed"}
 
     if args.impl == "reference":
@@ -295,7 +299,8 @@ def main():
 
     dt = float(__import__("synth").dt_for())
 
-    def mk(store, mode="swb", codec="blockquant", profile=False, resident_velocity=False):
+    def mk(store, mode="swb", codec=None, profile=False, resident_velocity=False):
+        codec = codec or args.codec
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
                              rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule)

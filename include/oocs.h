@@ -69,7 +69,8 @@ typedef enum {
 
 typedef enum {
     OOCS_CODEC_IDENTITY = 0,   /* raw fp32 (rate 32) */
-    OOCS_CODEC_BLOCKQUANT = 1  /* fixed-rate 4x4x4 block quantiser, rate_bits in [2, 24] */
+    OOCS_CODEC_BLOCKQUANT = 1, /* fixed-rate 4x4x4 block quantiser, rate_bits in [2, 24] */
+    OOCS_CODEC_ZFP = 2         /* ZFP fixed-rate (cuZFP's algorithm), rate_bits in [1, 32]; record = 8*rate B */
 } oocs_codec;
 
 /* Pipeline architectures of the paper (Fig. 6 `fig:3ver`, Fig. 7 `fig:swb`). */

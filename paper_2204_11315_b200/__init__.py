@@ -34,7 +34,7 @@ XOFF = 32 - R
 OOCS_OK = 0
 STATUS = {0: "OK", 2: "CONFIG", 3: "DEVICE_OOM", 4: "VERIFY", 5: "IO", 6: "DATA", 7: "HOST_OOM",
           8: "CUDA", 9: "EXCHANGE", 10: "STATE"}
-CODEC = {"identity": 0, "blockquant": 1}
+CODEC = {"identity": 0, "blockquant": 1, "zfp": 2}
 MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
 STORE = {"host": 0, "device": 1}
 SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}

@@ -475,6 +475,312 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
 }
 
 // ---------------------------------------------------------------------------
+// ZFP fixed-rate codec (NEXT-1; the algorithm of cuZFP), one thread per 4x4x4 block,
+// everything in registers: block-floating-point -> integer lifting along x, y, z -> sequency order
+// + negabinary -> a 2 x (32x32) in-register bit transpose turns the 64 coefficients into 32 bit
+// planes -> embedded coding with group tests, truncated at maxbits = 64 * rate.  Bit-exact with
+// oracle_zfp_encode_block / oracle_zfp_decode_block.
+// ---------------------------------------------------------------------------
+// compile-time copy (register renaming needs constant indices)
+struct ZfpPerm {
+    unsigned char p[64];
+};
+__host__ __device__ constexpr ZfpPerm zfp_perm() {
+    return ZfpPerm{{0,  1,  4,  16, 20, 17, 5,  2,  8,  32, 21, 6,  18, 24, 9,  33, 36, 3,  12, 48, 22, 25,
+                    37, 40, 34, 10, 7,  19, 28, 13, 49, 52, 41, 38, 26, 23, 29, 53, 11, 35, 44, 14, 50, 56,
+                    42, 27, 39, 45, 30, 54, 57, 60, 51, 15, 43, 46, 58, 61, 55, 31, 62, 59, 47, 63}};
+}
+
+__device__ __forceinline__ void zfp_fwd_lift(int32_t &x, int32_t &y, int32_t &z, int32_t &w) {
+    x += w; x >>= 1; w -= x;
+    z += y; z >>= 1; y -= z;
+    x += z; x >>= 1; z -= x;
+    w += y; w >>= 1; y -= w;
+    w += y >> 1; y -= w >> 1;
+}
+__device__ __forceinline__ void zfp_inv_lift(int32_t &x, int32_t &y, int32_t &z, int32_t &w) {
+    y += w >> 1; w -= y >> 1;
+    y += w; w <<= 1; w -= y;
+    z += x; x <<= 1; x -= z;
+    y += z; z <<= 1; z -= y;
+    w += x; x <<= 1; x -= w;
+}
+__device__ __forceinline__ void zfp_fwd_xform(int32_t (&b)[64]) {
+#pragma unroll
+    for (int z = 0; z < 4; z++)
+#pragma unroll
+        for (int y = 0; y < 4; y++) {
+            const int o = 4 * y + 16 * z;
+            zfp_fwd_lift(b[o], b[o + 1], b[o + 2], b[o + 3]);
+        }
+#pragma unroll
+    for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int z = 0; z < 4; z++) {
+            const int o = 16 * z + x;
+            zfp_fwd_lift(b[o], b[o + 4], b[o + 8], b[o + 12]);
+        }
+#pragma unroll
+    for (int y = 0; y < 4; y++)
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            const int o = x + 4 * y;
+            zfp_fwd_lift(b[o], b[o + 16], b[o + 32], b[o + 48]);
+        }
+}
+__device__ __forceinline__ void zfp_inv_xform(int32_t (&b)[64]) {
+#pragma unroll
+    for (int y = 0; y < 4; y++)
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            const int o = x + 4 * y;
+            zfp_inv_lift(b[o], b[o + 16], b[o + 32], b[o + 48]);
+        }
+#pragma unroll
+    for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int z = 0; z < 4; z++) {
+            const int o = 16 * z + x;
+            zfp_inv_lift(b[o], b[o + 4], b[o + 8], b[o + 12]);
+        }
+#pragma unroll
+    for (int z = 0; z < 4; z++)
+#pragma unroll
+        for (int y = 0; y < 4; y++) {
+            const int o = 4 * y + 16 * z;
+            zfp_inv_lift(b[o], b[o + 1], b[o + 2], b[o + 3]);
+        }
+}
+
+// in-register 32x32 bit transpose (LSB convention): afterwards bit j of a[k] = old bit k of a[j]
+__device__ __forceinline__ void transpose32_regs(uint32_t *a) {
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = s == 0 ? 0x0000FFFFu : s == 1 ? 0x00FF00FFu : s == 2 ? 0x0F0F0F0Fu
+                         : s == 3 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            if (r & j) continue;
+            const uint32_t t = ((a[r] >> j) ^ a[r | j]) & m;
+            a[r] ^= t << j;
+            a[r | j] ^= t;
+        }
+    }
+}
+
+struct BitWriter {
+    uint64_t *out;
+    uint64_t cur;
+    int nb;  // bits pending in cur
+    __device__ __forceinline__ void put1(uint32_t b) {
+        cur |= (uint64_t)(b & 1u) << nb;
+        if (++nb == 64) {
+            *out++ = cur;
+            cur = 0;
+            nb = 0;
+        }
+    }
+    __device__ __forceinline__ void put(uint64_t v, int m) {  // low m bits of v, 0 <= m <= 64
+        if (m == 0) return;
+        if (m < 64) v &= ((uint64_t)1 << m) - 1;
+        cur |= v << nb;
+        const int t = nb + m;
+        if (t >= 64) {
+            *out++ = cur;
+            cur = nb ? v >> (64 - nb) : 0;
+            nb = t - 64;
+        } else {
+            nb = t;
+        }
+    }
+};
+
+struct BitReader {
+    const uint64_t *in;
+    uint64_t cur;
+    int nb;  // unread bits left in cur
+    __device__ __forceinline__ uint32_t get1() {
+        if (nb == 0) {
+            cur = __ldg(in++);
+            nb = 64;
+        }
+        const uint32_t b = (uint32_t)(cur & 1u);
+        cur >>= 1;
+        --nb;
+        return b;
+    }
+    __device__ __forceinline__ uint64_t get(int m) {  // 0 <= m <= 64
+        if (m == 0) return 0;
+        uint64_t v;
+        if (m <= nb) {
+            v = m == 64 ? cur : cur & (((uint64_t)1 << m) - 1);
+            cur = m == 64 ? 0 : cur >> m;
+            nb -= m;
+        } else {
+            v = cur;
+            const int have = nb;
+            cur = __ldg(in++);
+            const int need = m - have;
+            v |= (need == 64 ? cur : (cur & (((uint64_t)1 << need) - 1))) << have;
+            cur = need == 64 ? 0 : cur >> need;
+            nb = 64 - need;
+        }
+        return v;
+    }
+};
+
+__device__ __forceinline__ uint32_t zfp_int2uint(int32_t x) { return ((uint32_t)x + 0xaaaaaaaau) ^ 0xaaaaaaaau; }
+__device__ __forceinline__ int32_t zfp_uint2int(uint32_t x) { return (int32_t)((x ^ 0xaaaaaaaau) - 0xaaaaaaaau); }
+
+// warp layout: blockIdx.y = block row (by + nby * bz), lanes over 32 x-adjacent blocks
+__global__ void __launch_bounds__(128)
+zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int nbx, int nby, int64_t pitch,
+                  int64_t pstride, int rate, int *err) {
+    const int bx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bx >= nbx) return;
+    const int by = blockIdx.y % nby, bz = blockIdx.y / nby;
+    const int words = rate;  // 64 * rate bits
+    uint64_t *rec = dst + ((int64_t)(bz * nby + by) * nbx + bx) * words;
+    float x[64];
+    const float *s0 = src + (int64_t)(4 * bz) * pstride + (int64_t)(4 * by) * pitch + XOFF + 4 * bx;
+#pragma unroll
+    for (int zi = 0; zi < 4; ++zi)
+#pragma unroll
+        for (int yi = 0; yi < 4; ++yi) {
+            const float4 v = __ldcs(reinterpret_cast<const float4 *>(s0 + (int64_t)zi * pstride + (int64_t)yi * pitch));
+            x[16 * zi + 4 * yi + 0] = v.x;
+            x[16 * zi + 4 * yi + 1] = v.y;
+            x[16 * zi + 4 * yi + 2] = v.z;
+            x[16 * zi + 4 * yi + 3] = v.w;
+        }
+    float amax = 0.f;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+        bad |= !(fabsf(x[j]) <= 3.402823466e38f);  // NaN or Inf
+        amax = fmaxf(amax, fabsf(x[j]));
+    }
+    if (bad) {
+        atomicOr(err, 1);
+        return;
+    }
+    BitWriter bw{rec, 0, 0};
+    int written = 0;
+    if (amax > 0.f) {
+        const int be = (int)(__float_as_uint(amax) >> 23);
+        const int emax = max(be - 126, -126);  // frexp exponent, clamped for denormals
+        const uint32_t e = (uint32_t)(emax + 127);
+        bw.put(2 * (uint64_t)e + 1, 9);
+        int32_t ib[64];
+        if (emax >= -97) {  // 2^(30-emax) is a normal float: the float product is exact
+            const float sc = __int_as_float((127 + 30 - emax) << 23);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) ib[j] = (int32_t)(sc * x[j]);
+        } else {
+            const double sc = ldexp(1.0, 30 - emax);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) ib[j] = (int32_t)(sc * (double)x[j]);
+        }
+        zfp_fwd_xform(ib);
+        constexpr ZfpPerm P = zfp_perm();
+        uint32_t pl[64];  // coefficients in sequency order, negabinary; transposed into bit planes
+#pragma unroll
+        for (int i = 0; i < 64; ++i) pl[i] = zfp_int2uint(ib[P.p[i]]);
+        transpose32_regs(pl);       // pl[k]      bit j = bit k of coefficient j       (j < 32)
+        transpose32_regs(pl + 32);  // pl[32 + k] bit j = bit k of coefficient 32 + j
+        int bits = 64 * rate - 9;
+        int n = 0;
+#pragma unroll
+        for (int k = 31; k >= 0; --k) {
+            if (bits <= 0) break;
+            uint64_t plane = (uint64_t)pl[k] | ((uint64_t)pl[32 + k] << 32);
+            const int m = min(n, bits);
+            bits -= m;
+            bw.put(plane, m);
+            plane = m == 64 ? 0 : plane >> m;
+            for (; n < 64 && bits > 0; plane >>= 1, n++) {
+                bits--;
+                bw.put1(plane != 0);
+                if (!plane) break;
+                for (; n < 63 && bits > 0; plane >>= 1, n++) {
+                    bits--;
+                    bw.put1((uint32_t)plane);
+                    if (plane & 1u) break;
+                }
+            }
+        }
+        written = 64 * rate - bits;
+    } else {
+        bw.put1(0);
+        written = 1;
+    }
+    (void)written;
+    // pad the record with zeros up to maxbits
+    if (bw.nb) *bw.out++ = bw.cur;
+    while (bw.out < rec + words) *bw.out++ = 0;
+}
+
+__global__ void __launch_bounds__(128)
+zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int nbx, int nby, int64_t pitch,
+                  int64_t pstride, int rate) {
+    const int bx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bx >= nbx) return;
+    const int by = blockIdx.y % nby, bz = blockIdx.y / nby;
+    const uint64_t *rec = src + ((int64_t)(bz * nby + by) * nbx + bx) * rate;
+    BitReader br{rec, 0, 0};
+    float x[64];
+    if (!br.get1()) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) x[j] = 0.f;
+    } else {
+        const int emax = (int)br.get(8) - 127;
+        uint32_t pl[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) pl[i] = 0;
+        int bits = 64 * rate - 9;
+        int n = 0;
+#pragma unroll
+        for (int k = 31; k >= 0; --k) {
+            if (bits <= 0) break;
+            const int m = min(n, bits);
+            bits -= m;
+            uint64_t plane = br.get(m);
+            for (; n < 64 && bits > 0;) {
+                bits--;
+                if (!br.get1()) break;
+                for (; n < 63 && bits > 0; n++) {
+                    bits--;
+                    if (br.get1()) break;
+                }
+                plane += (uint64_t)1 << n;
+                n++;
+            }
+            pl[k] = (uint32_t)plane;
+            pl[32 + k] = (uint32_t)(plane >> 32);
+        }
+        transpose32_regs(pl);       // back to coefficients: pl[j] bit k = plane k bit j
+        transpose32_regs(pl + 32);
+        constexpr ZfpPerm P = zfp_perm();
+        int32_t ib[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) ib[P.p[i]] = zfp_uint2int(pl[i]);
+        zfp_inv_xform(ib);
+        const double sc = ldexp(1.0, emax - 30);
+#pragma unroll
+        for (int j = 0; j < 64; ++j) x[j] = (float)((double)__int2float_rn(ib[j]) * sc);
+    }
+    float *d0 = dst + (int64_t)(4 * bz) * pstride + (int64_t)(4 * by) * pitch + XOFF + 4 * bx;
+#pragma unroll
+    for (int zi = 0; zi < 4; ++zi)
+#pragma unroll
+        for (int yi = 0; yi < 4; ++yi)
+            __stcs(reinterpret_cast<float4 *>(d0 + (int64_t)zi * pstride + (int64_t)yi * pitch),
+                   make_float4(x[16 * zi + 4 * yi], x[16 * zi + 4 * yi + 1], x[16 * zi + 4 * yi + 2],
+                               x[16 * zi + 4 * yi + 3]));
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static inline int64_t nlines_of(int64_t ax) { return (XOFF + ax + 31) / 32; }
@@ -483,6 +789,12 @@ cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, i
                           int codec, int q, cudaStream_t st) {
     if (planes <= 0) return cudaSuccess;
     const int64_t pstride = ay * pitch;
+    if (codec == 2) {  // ZFP: q carries the rate
+        const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+        const dim3 grid((unsigned)((nbx + 127) / 128), (unsigned)(nby * (planes / 4)));
+        zfp_decode_kernel<<<grid, 128, 0, st>>>(static_cast<const uint64_t *>(src), dst, nbx, nby, pitch, pstride, q);
+        return cudaGetLastError();
+    }
     if (codec == 0) {
         const int64_t n4 = planes * ay * (ax / 4);
         const int threads = 256;
@@ -513,6 +825,12 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
                           int codec, int q, int *err, cudaStream_t st) {
     if (planes <= 0) return cudaSuccess;
     const int64_t pstride = ay * pitch;
+    if (codec == 2) {  // ZFP: q carries the rate
+        const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+        const dim3 grid((unsigned)((nbx + 127) / 128), (unsigned)(nby * (planes / 4)));
+        zfp_encode_kernel<<<grid, 128, 0, st>>>(src, static_cast<uint64_t *>(dst), nbx, nby, pitch, pstride, q, err);
+        return cudaGetLastError();
+    }
     if (codec == 0) {
         const int64_t n4 = planes * ay * (ax / 4);
         const int threads = 256;

@@ -781,29 +781,31 @@ oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out) {
 
 oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
                         int32_t codec, int32_t rate_bits, void *stream) {
-    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || (codec != 0 && codec != 1) ||
-        (codec == 1 && (rate_bits < 2 || rate_bits > 24))) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 2 ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32))) {
         set_error("oocs_decode: bad geometry or codec");
         return OOCS_ERR_CONFIG;
     }
-    CU(launch_decode(src, dst, ax, ay, planes, pitch, codec, codec ? rate_bits - 1 : 0, (cudaStream_t)stream));
+    const int qk = codec == 1 ? rate_bits - 1 : codec == 2 ? rate_bits : 0;
+    CU(launch_decode(src, dst, ax, ay, planes, pitch, codec, qk, (cudaStream_t)stream));
     return OOCS_OK;
 }
 
 oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
                         int32_t codec, int32_t rate_bits, int32_t *err_flag, void *stream) {
-    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || (codec != 0 && codec != 1) ||
-        (codec == 1 && (rate_bits < 2 || rate_bits > 24))) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 2 ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32))) {
         set_error("oocs_encode: bad geometry or codec");
         return OOCS_ERR_CONFIG;
     }
+    const int qk = codec == 1 ? rate_bits - 1 : codec == 2 ? rate_bits : 0;
     int *flag = err_flag;
     static int *dummy = nullptr;  // per-process scratch flag when the caller passes NULL
     if (!flag) {
         if (!dummy) CU(cudaMalloc((void **)&dummy, sizeof(int)));
         flag = dummy;
     }
-    CU(launch_encode(src, dst, ax, ay, planes, pitch, codec, codec ? rate_bits - 1 : 0, flag, (cudaStream_t)stream));
+    CU(launch_encode(src, dst, ax, ay, planes, pitch, codec, qk, flag, (cudaStream_t)stream));
     return OOCS_OK;
 }
 

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=4096)
     ap.add_argument("--ks", default="1,4")
     ap.add_argument("--rates", default="8,12,16,24")
+    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_accuracy.json"))
     a = ap.parse_args()
     n, nb = a.n, a.nb
@@ -44,7 +45,7 @@ def main():
         bench.load_state(ref, n, n, n, 0)
         lossy = {}
         for r in [int(x) for x in a.rates.split(",")]:
-            lossy[r] = mk("blockquant", r)
+            lossy[r] = mk(a.codec, r)
             bench.load_state(lossy[r], n, n, n, 0)
         done = 0
         for c in checkpoints:
@@ -57,7 +58,7 @@ def main():
                 pg = pl.store(2, 0, az).astype(np.float64)[R:-R, R:-R, R:-R]
                 err = pg - pr
                 rmse = float(np.sqrt(np.mean(err ** 2)))
-                row = {"n": n, "k": k, "rate": r, "steps": c, "max_abs_err": float(np.abs(err).max()),
+                row = {"n": n, "k": k, "codec": a.codec, "rate": r, "steps": c, "max_abs_err": float(np.abs(err).max()),
                        "rmse": rmse, "psnr_db": float(20 * np.log10(span / rmse)) if rmse > 0 else None,
                        "ref_range": float(span), "ref_max_abs": float(np.abs(pr).max())}
                 rows.append(row)
