@@ -598,48 +598,45 @@ struct BitWriter {
 
 struct BitReader {
     const uint64_t *in;
-    uint64_t cur;
-    int nb;  // unread bits left in cur
-    __device__ __forceinline__ uint32_t get1() {
-        if (nb == 0) {
-            cur = __ldg(in++);
-            nb = 64;
-        }
-        const uint32_t b = (uint32_t)(cur & 1u);
-        cur >>= 1;
-        --nb;
-        return b;
+    uint64_t cur;  // the nb unconsumed bits, LSB first (higher bits zero)
+    int nb;
+    __device__ __forceinline__ uint64_t peek(int m) const {  // next m bits (1 <= m <= 64), not consumed
+        uint64_t v = cur;
+        if (m > nb) v |= __ldg(in) << nb;  // nb < 64 here
+        return m == 64 ? v : v & (((uint64_t)1 << m) - 1);
     }
-    __device__ __forceinline__ uint64_t get(int m) {  // 0 <= m <= 64
-        if (m == 0) return 0;
-        uint64_t v;
-        if (m <= nb) {
-            v = m == 64 ? cur : cur & (((uint64_t)1 << m) - 1);
-            cur = m == 64 ? 0 : cur >> m;
+    __device__ __forceinline__ void skip(int m) {  // consume m bits (0 <= m <= 64)
+        if (m < nb) {
+            cur >>= m;
             nb -= m;
         } else {
-            v = cur;
-            const int have = nb;
-            cur = __ldg(in++);
-            const int need = m - have;
-            v |= (need == 64 ? cur : (cur & (((uint64_t)1 << need) - 1))) << have;
-            cur = need == 64 ? 0 : cur >> need;
-            nb = 64 - need;
+            const int r = m - nb;
+            const uint64_t w = __ldg(in++);
+            cur = r == 64 ? 0 : w >> r;
+            nb = 64 - r;
         }
+    }
+    __device__ __forceinline__ uint64_t get(int m) {
+        if (m == 0) return 0;
+        const uint64_t v = peek(m);
+        skip(m);
         return v;
     }
+    __device__ __forceinline__ uint32_t get1() { return (uint32_t)get(1); }
 };
 
 __device__ __forceinline__ uint32_t zfp_int2uint(int32_t x) { return ((uint32_t)x + 0xaaaaaaaau) ^ 0xaaaaaaaau; }
 __device__ __forceinline__ int32_t zfp_uint2int(uint32_t x) { return (int32_t)((x ^ 0xaaaaaaaau) - 0xaaaaaaaau); }
 
-// warp layout: blockIdx.y = block row (by + nby * bz), lanes over 32 x-adjacent blocks
+// grid: x over the (by, bx) blocks of a slab (one thread each), y = slab
 __global__ void __launch_bounds__(128)
 zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int nbx, int nby, int64_t pitch,
                   int64_t pstride, int rate, int *err) {
-    const int bx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (bx >= nbx) return;
-    const int by = blockIdx.y % nby, bz = blockIdx.y / nby;
+    __shared__ uint64_t zs_planes[32][128];
+    // one thread per block, flattened over the slab's (by, bx) so no lanes idle at row ends
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nbx * nby) return;
+    const int bx = (int)(t % nbx), by = (int)(t / nbx), bz = blockIdx.y;
     const int words = rate;  // 64 * rate bits
     uint64_t *rec = dst + ((int64_t)(bz * nby + by) * nbx + bx) * words;
     float x[64];
@@ -666,7 +663,6 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
         return;
     }
     BitWriter bw{rec, 0, 0};
-    int written = 0;
     if (amax > 0.f) {
         const int be = (int)(__float_as_uint(amax) >> 23);
         const int emax = max(be - 126, -126);  // frexp exponent, clamped for denormals
@@ -689,33 +685,45 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
         for (int i = 0; i < 64; ++i) pl[i] = zfp_int2uint(ib[P.p[i]]);
         transpose32_regs(pl);       // pl[k]      bit j = bit k of coefficient j       (j < 32)
         transpose32_regs(pl + 32);  // pl[32 + k] bit j = bit k of coefficient 32 + j
+        // bit planes to shared memory ([plane][thread]: conflict-free), so the data-dependent coding
+        // loop below stays rolled (a 32x unrolled loop overflows the instruction cache)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) zs_planes[k][threadIdx.x] = (uint64_t)pl[k] | ((uint64_t)pl[32 + k] << 32);
         int bits = 64 * rate - 9;
         int n = 0;
-#pragma unroll
+#pragma unroll 1
         for (int k = 31; k >= 0; --k) {
             if (bits <= 0) break;
-            uint64_t plane = (uint64_t)pl[k] | ((uint64_t)pl[32 + k] << 32);
+            uint64_t plane = zs_planes[k][threadIdx.x];
             const int m = min(n, bits);
             bits -= m;
             bw.put(plane, m);
             plane = m == 64 ? 0 : plane >> m;
-            for (; n < 64 && bits > 0; plane >>= 1, n++) {
+            // unary run-length code of the remainder, one step per newly significant coefficient:
+            // group test bit, then the zeros up to the next 1 and that 1 (implied at position 63)
+            while (n < 64 && bits > 0) {
                 bits--;
                 bw.put1(plane != 0);
                 if (!plane) break;
-                for (; n < 63 && bits > 0; plane >>= 1, n++) {
-                    bits--;
-                    bw.put1((uint32_t)plane);
-                    if (plane & 1u) break;
+                const int z = __ffsll((long long)plane) - 1, zmax = 63 - n;
+                const int len = z < zmax ? z + 1 : zmax;  // bits the zfp loop would write
+                if (len <= bits) {
+                    bw.put(z < zmax ? (uint64_t)1 << z : 0, len);
+                    bits -= len;
+                    const int adv = z < zmax ? z + 1 : zmax + 1;
+                    n += adv;
+                    plane = adv >= 64 ? 0 : plane >> adv;
+                } else {  // budget ends inside the zero run
+                    bw.put(0, bits);
+                    n += bits + 1;
+                    plane = 0;
+                    bits = 0;
                 }
             }
         }
-        written = 64 * rate - bits;
     } else {
         bw.put1(0);
-        written = 1;
     }
-    (void)written;
     // pad the record with zeros up to maxbits
     if (bw.nb) *bw.out++ = bw.cur;
     while (bw.out < rec + words) *bw.out++ = 0;
@@ -724,9 +732,10 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
 __global__ void __launch_bounds__(128)
 zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int nbx, int nby, int64_t pitch,
                   int64_t pstride, int rate) {
-    const int bx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (bx >= nbx) return;
-    const int by = blockIdx.y % nby, bz = blockIdx.y / nby;
+    __shared__ uint64_t zs_planes[32][128];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nbx * nby) return;
+    const int bx = (int)(t % nbx), by = (int)(t / nbx), bz = blockIdx.y;
     const uint64_t *rec = src + ((int64_t)(bz * nby + by) * nbx + bx) * rate;
     BitReader br{rec, 0, 0};
     float x[64];
@@ -735,27 +744,42 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
         for (int j = 0; j < 64; ++j) x[j] = 0.f;
     } else {
         const int emax = (int)br.get(8) - 127;
-        uint32_t pl[64];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) pl[i] = 0;
+        for (int k = 0; k < 32; ++k) zs_planes[k][threadIdx.x] = 0;
         int bits = 64 * rate - 9;
         int n = 0;
-#pragma unroll
+#pragma unroll 1
         for (int k = 31; k >= 0; --k) {
             if (bits <= 0) break;
             const int m = min(n, bits);
             bits -= m;
             uint64_t plane = br.get(m);
-            for (; n < 64 && bits > 0;) {
+            while (n < 64 && bits > 0) {
                 bits--;
                 if (!br.get1()) break;
-                for (; n < 63 && bits > 0; n++) {
-                    bits--;
-                    if (br.get1()) break;
+                const int avail = min(63 - n, bits);  // zeros the zfp loop may read before stopping
+                int z = avail;
+                if (avail > 0) {
+                    const uint64_t look = br.peek(avail);
+                    if (look) z = __ffsll((long long)look) - 1;
                 }
+                if (z < avail) {  // a 1 at position n + z
+                    br.skip(z + 1);
+                    bits -= z + 1;
+                } else {          // n reached 63 (its 1 is implied) or the budget ended
+                    br.skip(avail);
+                    bits -= avail;
+                }
+                n += z;
                 plane += (uint64_t)1 << n;
                 n++;
             }
+            zs_planes[k][threadIdx.x] = plane;
+        }
+        uint32_t pl[64];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint64_t plane = zs_planes[k][threadIdx.x];
             pl[k] = (uint32_t)plane;
             pl[32 + k] = (uint32_t)(plane >> 32);
         }
@@ -791,7 +815,7 @@ cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, i
     const int64_t pstride = ay * pitch;
     if (codec == 2) {  // ZFP: q carries the rate
         const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-        const dim3 grid((unsigned)((nbx + 127) / 128), (unsigned)(nby * (planes / 4)));
+        const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
         zfp_decode_kernel<<<grid, 128, 0, st>>>(static_cast<const uint64_t *>(src), dst, nbx, nby, pitch, pstride, q);
         return cudaGetLastError();
     }
@@ -827,7 +851,7 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
     const int64_t pstride = ay * pitch;
     if (codec == 2) {  // ZFP: q carries the rate
         const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-        const dim3 grid((unsigned)((nbx + 127) / 128), (unsigned)(nby * (planes / 4)));
+        const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
         zfp_encode_kernel<<<grid, 128, 0, st>>>(src, static_cast<uint64_t *>(dst), nbx, nby, pitch, pstride, q, err);
         return cudaGetLastError();
     }
