@@ -1,0 +1,27 @@
+"""Small runs of every hot-path kernel and schedule for compute-sanitizer (memcheck / racecheck /
+synccheck): ragged grids, BlockQuant and ZFP, host and device stores, Alg. 1 and DAG schedules."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2204_11315_b200 as oocs  # noqa: E402
+import synth  # noqa: E402
+
+R = 4
+nx, ny, nz = 44, 36, 48
+vel, p0 = synth.fields(nx, ny, nz)
+az = nz + 2 * R
+for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("identity", 32)):
+    for store, sched, mode in (("host", "alg1", "swb"), ("device", "alg1", "swb"), ("host", "dag_func", "dwb")):
+        c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=3, tb_depth=2, codec=codec,
+                             rate_bits=rate, mode=mode, store=store, schedule=sched)
+        pl = oocs.Plan(c)
+        for a, arr in enumerate((vel, p0, p0)):
+            pl.load(a, arr, 0, az)
+        pl.run(4)
+        out = pl.store(2, 0, az)
+        assert np.isfinite(out).all()
+        pl.close()
+        print("ok", codec, rate, store, sched, mode, flush=True)
