@@ -71,7 +71,6 @@ __device__ __forceinline__ LineTask line_task(int nbx) {
 }
 
 constexpr int CODEC_WARPS = 8;
-constexpr int TILE_LD = 36;  // padded row (floats): conflict-free scatter of 4x4 block rows
 constexpr int CODE_LD = 68;  // padded per-block code row (u32)
 
 // ---------------------------------------------------------------------------
@@ -84,7 +83,7 @@ __global__ void __launch_bounds__(CODEC_WARPS * 32)
 bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int nbx, int nby,
                  int64_t pitch, int64_t pstride, int q_rt) {
     const int q = QT ? QT : q_rt;
-    __shared__ __align__(16) float tile[CODEC_WARPS][16][TILE_LD];
+    __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const LineTask t = line_task(nbx);
     if (t.by >= nby) return;
@@ -106,14 +105,11 @@ bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int n
     const float mn_l = __uint_as_float(hdr);
     const float step_l = __fmul_rn(__fsub_rn(mx_l, mn_l), pow2f(-q));  // valid on lanes 0..7
     const Xpose X(lane);
-    const int xi = lane & 3, yi = (lane >> 2) & 3, zi = lane >> 4;
-    float(*tl)[TILE_LD] = tile[warp];
-    // blocks i >= nb (line ends) decode zeros into tile columns that are never written out;
-    // keeping the loop unconditional keeps every shuffle warp-convergent
+    uint32_t(*cw)[CODE_LD] = codes[warp];
+    // blocks i >= nb (line ends) decode zeros that are never written out; keeping the loop
+    // unconditional keeps every shuffle warp-convergent
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const float mn = __shfl_sync(0xffffffffu, mn_l, i);
-        const float step = __shfl_sync(0xffffffffu, step_l, i);
         const uint32_t y0 = X(w0[i]);
         uint32_t c_lo = y0 & 0xFFFFu, c_hi = y0 >> 16;
         if (TWO) {
@@ -121,18 +117,26 @@ bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int n
             c_lo |= (y1 & 0xFFFFu) << 16;
             c_hi |= (y1 >> 16) << 16;
         }
-        tl[yi + 4 * zi][4 * i + xi] = __fmaf_rn(__fadd_rn(__uint2float_rn(c_lo), 0.5f), step, mn);
-        tl[yi + 4 * (zi + 2)][4 * i + xi] = __fmaf_rn(__fadd_rn(__uint2float_rn(c_hi), 0.5f), step, mn);
+        cw[i][lane] = c_lo;
+        cw[i][lane + 32] = c_hi;
     }
     __syncwarp();
-    const int col0 = XOFF + 4 * t.b0;
-    float *dbase = dst + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + col0;
+    // reconstruct in the store layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12 (code j = xi + 4r),
+    // each row one aligned float4: per instruction 4 rows x 128 contiguous bytes
+    const int ib = lane & 7, r0 = lane >> 3;
+    const float mn = __shfl_sync(0xffffffffu, mn_l, ib), step = __shfl_sync(0xffffffffu, step_l, ib);
+    float *dbase = dst + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
+    if (ib < t.nb) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // 16 rows x 8 float4: row r = f >> 3, block c = f & 7
-        const int f = lane + 32 * u, r = f >> 3, c = f & 7;
-        if (c < t.nb)
-            __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch + 4 * c),
-                   *reinterpret_cast<const float4 *>(&tl[r][4 * c]));
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + 4 * u;
+            const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
+            const float4 v = make_float4(__fmaf_rn(__fadd_rn(__uint2float_rn(c.x), 0.5f), step, mn),
+                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.y), 0.5f), step, mn),
+                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.z), 0.5f), step, mn),
+                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.w), 0.5f), step, mn));
+            __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch), v);
+        }
     }
 }
 
@@ -148,30 +152,22 @@ __global__ void __launch_bounds__(CODEC_WARPS * 32)
 bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int nbx, int nby,
                  int64_t pitch, int64_t pstride, int q_rt, int *err) {
     const int q = QT ? QT : q_rt;
-    __shared__ __align__(16) float tile[CODEC_WARPS][16][TILE_LD];
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const LineTask t = line_task(nbx);
     if (t.by >= nby) return;
-    float(*tl)[TILE_LD] = tile[warp];
-    const int col0 = XOFF + 4 * t.b0;
-    const float *sbase = src + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + col0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {  // 16 rows x 8 float4: row r = f >> 3, block c = f & 7
-        const int f = lane + 32 * u, r = f >> 3, c = f & 7;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < t.nb)
-            x = __ldcs(reinterpret_cast<const float4 *>(sbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch +
-                                                        4 * c));
-        *reinterpret_cast<float4 *>(&tl[r][4 * c]) = x;
-    }
-    __syncwarp();
-    // ---- per-block statistics and codes: lane -> block ib, rows r0, r0+4, r0+8, r0+12
+    // ---- load straight into the statistics layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12
+    //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging)
     const int ib = lane & 7, r0 = lane >> 3;
     const bool live = ib < t.nb;
+    const float *sbase = src + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
     float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4 *>(&tl[r0 + 4 * u][4 * ib]);
+    for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 4 * u;  // r = yi + 4 zi
+        v[u] = live ? __ldcs(reinterpret_cast<const float4 *>(sbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float mn = v[0].x, mx = v[0].x;
     bool nan = false;
 #pragma unroll
