@@ -27,7 +27,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liboocs.so")
+LIB_PATH = os.environ.get("OOCS_LIB", os.path.join(HERE, "liboocs.so"))  # override: experiments only
 R = 4
 XOFF = 32 - R
 

@@ -310,3 +310,30 @@ def test_device_oom_and_bad_steps():
     with pytest.raises(oocs.OocsError) as e:
         pl.load(1, bad, 0, 40)
     assert e.value.status == 6
+
+
+def test_degenerate_cases():
+    """steps = 0 leaves the state bitwise unchanged; the smallest legal grid (4^3 interior, 2 chunks of
+    8 planes, k = 1); a single chunk spanning the whole domain; all with the lossy codec."""
+    vel, p0 = synth.fields(4, 4, 16)
+    az = 16 + 2 * R
+    pl = make_plan(4, 4, 16, 2, 1, rate=16)
+    load_fields(pl, vel, p0)
+    before = pl.read_raw(2, 0, az)
+    st = pl.run(0)
+    assert st.cell_updates == 0 and np.array_equal(pl.read_raw(2, 0, az), before)
+    pl.run(3)
+    S = [oracle.encode_planes(a, 1, 15) for a in (vel, p0, p0)]
+    oracle.pipeline(12, 12, 16, 2, 1, synth.dt_for(), 3, 1, 15, *S)
+    got = oracle.decode_planes(pl.read_raw(2, 0, az), 12, 12, az, 1, 15)
+    want = oracle.decode_planes(S[2], 12, 12, az, 1, 15)
+    assert np.max(np.abs(got - want)) < 1e-4
+    pl.close()
+    # one chunk = the whole domain (no carry, both physical boundaries in one extent)
+    vel, p0 = synth.fields(16, 16, 32)
+    a1 = make_plan(16, 16, 32, 1, 2, codec="identity")
+    load_fields(a1, vel, p0)
+    a1.run(4)
+    _, pc = oracle.incore(vel, p0.copy(), p0.copy(), synth.dt_for(), 4)
+    assert _rel_err(a1.store(2, 0, 40), pc.astype(np.float64)) <= 4e-6
+    a1.close()
