@@ -250,7 +250,7 @@ __global__ void id_encode_kernel(const float *__restrict__ src, float4 *__restri
 
 // ---------------------------------------------------------------------------
 // 25-point leapfrog step:
-//   p_prev <- 2 p_curr - p_prev + (v dt)^2 * (3 c0 f0 + sum_axes sum_m c_m (f(+m) + f(-m)))
+//   p_prev <- 2 p_curr - p_prev + (v dt)^2 * sum_axes sum_m c_m ((f(+m) + f(-m)) - 2 f0)
 //
 // 2.5-D blocking with a TMA pipeline.  A CTA owns a 64 x 16 xy tile and
 // marches a z range.  One thread issues cp.async.bulk.tensor loads, two
@@ -276,7 +276,6 @@ struct S2Smem {
 constexpr size_t S2_SMEM = sizeof(S2Smem);
 
 // coefficients of d2/dx2, order 8 (Q1): 8/5, -1/5, 8/315, -1/560
-#define C0X3 (-8.541666666666666f)  // 3 * (-205/72)
 #define C1 1.6f
 #define C2 (-0.2f)
 #define C3 0.025396825396825397f
@@ -385,20 +384,18 @@ __device__ __forceinline__ bool s2_plane(S2Smem &S, const CUtensorMap *mP, const
             const int cxi = 4 + i;  // column of the centre in xr
             const int ryi = 4 + r;  // row of the centre in yr
             auto yv = [&](int m) { return i ? yr[m].y : yr[m].x; };
-            // Lap25 = 3 c0 f0 + sum_axes sum_m c_m (f(+m) + f(-m)), accumulated with FMA in x, y, z order
-            float lap = __fmul_rn(C0X3, f0);
-            lap = __fmaf_rn(C1, __fadd_rn(xr[cxi - 1], xr[cxi + 1]), lap);
-            lap = __fmaf_rn(C2, __fadd_rn(xr[cxi - 2], xr[cxi + 2]), lap);
-            lap = __fmaf_rn(C3, __fadd_rn(xr[cxi - 3], xr[cxi + 3]), lap);
-            lap = __fmaf_rn(C4, __fadd_rn(xr[cxi - 4], xr[cxi + 4]), lap);
-            lap = __fmaf_rn(C1, __fadd_rn(yv(ryi - 1), yv(ryi + 1)), lap);
-            lap = __fmaf_rn(C2, __fadd_rn(yv(ryi - 2), yv(ryi + 2)), lap);
-            lap = __fmaf_rn(C3, __fadd_rn(yv(ryi - 3), yv(ryi + 3)), lap);
-            lap = __fmaf_rn(C4, __fadd_rn(yv(ryi - 4), yv(ryi + 4)), lap);
-            lap = __fmaf_rn(C1, __fadd_rn(q[(OFF + 3) % 9][ci], q[(OFF + 5) % 9][ci]), lap);
-            lap = __fmaf_rn(C2, __fadd_rn(q[(OFF + 2) % 9][ci], q[(OFF + 6) % 9][ci]), lap);
-            lap = __fmaf_rn(C3, __fadd_rn(q[(OFF + 1) % 9][ci], q[(OFF + 7) % 9][ci]), lap);
-            lap = __fmaf_rn(C4, __fadd_rn(q[(OFF + 0) % 9][ci], q[(OFF + 8) % 9][ci]), lap);
+            float lap = __fmul_rn(C1, __fsub_rn(__fadd_rn(xr[cxi - 1], xr[cxi + 1]), f2));
+            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(xr[cxi - 2], xr[cxi + 2]), f2), lap);
+            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(xr[cxi - 3], xr[cxi + 3]), f2), lap);
+            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(xr[cxi - 4], xr[cxi + 4]), f2), lap);
+            lap = __fmaf_rn(C1, __fsub_rn(__fadd_rn(yv(ryi - 1), yv(ryi + 1)), f2), lap);
+            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(yv(ryi - 2), yv(ryi + 2)), f2), lap);
+            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(yv(ryi - 3), yv(ryi + 3)), f2), lap);
+            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(yv(ryi - 4), yv(ryi + 4)), f2), lap);
+            lap = __fmaf_rn(C1, __fsub_rn(__fadd_rn(q[(OFF + 3) % 9][ci], q[(OFF + 5) % 9][ci]), f2), lap);
+            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(q[(OFF + 2) % 9][ci], q[(OFF + 6) % 9][ci]), f2), lap);
+            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(q[(OFF + 1) % 9][ci], q[(OFF + 7) % 9][ci]), f2), lap);
+            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(q[(OFF + 0) % 9][ci], q[(OFF + 8) % 9][ci]), f2), lap);
             const float vv = r ? (i ? v1.y : v1.x) : (i ? v0.y : v0.x);
             const float pv = r ? (i ? pp1.y : pp1.x) : (i ? pp0.y : pp0.x);
             const float vd = __fmul_rn(vv, a.dt);
