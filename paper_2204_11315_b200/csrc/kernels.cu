@@ -883,14 +883,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn encode_tiled() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
+    // resolved once, thread-safe (plans may be driven from several host threads)
+    static const EncodeTiledFn fn = [] {
         void *p = nullptr;
         cudaDriverEntryPointQueryResult qr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
             qr == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
+            return reinterpret_cast<EncodeTiledFn>(p);
+        return (EncodeTiledFn) nullptr;
+    }();
     return fn;
 }
 
@@ -909,13 +910,10 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t pitch, int64_t a
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st) {
     if (z_hi <= z_lo) return cudaSuccess;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)S2_SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // per device (the attribute is per function and device); idempotent, so racing threads are harmless
+    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)S2_SMEM);
+    if (e != cudaSuccess) return e;
     CUtensorMap mP, mPP, mV;
     if (!make_map(&mP, pcurr, pitch, ay, planes, S2_PW, S2_PH) || !make_map(&mPP, pprev, pitch, ay, planes, S2_TX, S2_TY) ||
         !make_map(&mV, vel, pitch, ay, planes, S2_TX, S2_TY))

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -256,7 +257,12 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
         return st;
     }
     const Geometry &g = p->geo;
-    CU(cudaSetDevice(g.cfg.device));
+    if (cudaSetDevice(g.cfg.device) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaSetDevice failed for the plan's device");
+        delete p;
+        return OOCS_ERR_CUDA;
+    }
     const Sizes z = compute_sizes(g);
     const size_t ws_array = z.ws_array, hfb = z.hfb, arr_store = z.arr_store, total = z.total;
     const bool codec_staging = z.codec_staging;
@@ -800,10 +806,19 @@ oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int
     }
     const int qk = codec == 1 ? rate_bits - 1 : codec == 2 ? rate_bits : 0;
     int *flag = err_flag;
-    static int *dummy = nullptr;  // per-process scratch flag when the caller passes NULL
     if (!flag) {
-        if (!dummy) CU(cudaMalloc((void **)&dummy, sizeof(int)));
-        flag = dummy;
+        // the caller does not want the flag: a per-device scratch word, allocated once
+        static std::mutex mu;
+        static int *scratch[64] = {};
+        int dev = 0;
+        CU(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 0 || dev >= 64) {
+            set_error("device ordinal out of range");
+            return OOCS_ERR_CONFIG;
+        }
+        if (!scratch[dev]) CU(cudaMalloc((void **)&scratch[dev], sizeof(int)));
+        flag = scratch[dev];
     }
     CU(launch_encode(src, dst, ax, ay, planes, pitch, codec, qk, flag, (cudaStream_t)stream));
     return OOCS_OK;
