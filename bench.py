@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--impl", default="oocs", choices=["oocs", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fuse-encode", action="store_true", help="fuse each chunk's last step with its encode "
+                    "(device store, BlockQuant; OOCS_FLAG_FUSE_ENCODE)")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
     ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp"],
                     help="fixed-rate codec of the compressed state (ZFP = NEXT-1)")
@@ -239,6 +241,7 @@ def main():
                 f"single working buffer")
     config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
               "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
+              "fused_last_step_encode": args.codec == "blockquant" and args.fuse_encode,
               "parallelism": f"z-slabs x{world}",
               "l2": "inputs larger than L2 (compressed state 6.6 GB/GPU >> 126 MB), no flush needed"}
 
@@ -303,7 +306,8 @@ def main():
         codec = codec or args.codec
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
                              rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
-                             profile=profile, resident_velocity=resident_velocity, schedule=args.schedule)
+                             profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
+                             fusion=args.fuse_encode)
         pl = oocs.Plan(c)
         if world > 1:
             pl.set_exchange((odist.gloo_exchange_fn if gloo else odist.nccl_exchange_fn)(rank, world))

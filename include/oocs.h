@@ -100,6 +100,11 @@ typedef enum {
  * P:L244) resident in HBM instead of re-sending it every sweep (SPEC S:L508's config flag);
  * H2D then moves the two pressure arrays only.  Off by default (paper-faithful accounting). */
 #define OOCS_FLAG_RESIDENT_VELOCITY 2u
+/* Device store + BlockQuant: fuse every chunk's last step with the encode of its owned planes (level
+ * k is never written back; the two time levels go straight into S_{t+1}).  Off by default: it moves
+ * 35% fewer HBM bytes than step + encode but is issue-bound and measures ~1.5%
+ * slower on B200.  Ignored by other modes. */
+#define OOCS_FLAG_FUSE_ENCODE 4u
 
 typedef struct {
     uint32_t struct_size;     /* sizeof(oocs_config): ABI versioning */

@@ -40,6 +40,7 @@ STORE = {"host": 0, "device": 1}
 SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}
 FLAG_PROFILE = 1
 FLAG_RESIDENT_VELOCITY = 2
+FLAG_FUSE_ENCODE = 4
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
 EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY", "NODE"]
 
@@ -141,7 +142,7 @@ def _check(st: int, where: str):
 
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
-                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1") -> Config:
+                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False) -> Config:
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -155,7 +156,8 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.schedule = SCHED[schedule] if isinstance(schedule, str) else schedule
     c.store = STORE[store] if isinstance(store, str) else store
     c.device, c.rank, c.world = device, rank, world
-    c.flags = (FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
+    c.flags = ((FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
+               | (FLAG_FUSE_ENCODE if fusion else 0))
     c.device_capacity = device_capacity
     return c
 

@@ -147,27 +147,15 @@ bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int n
 // Statistics and quantisation are vectorised over the warp's 8 blocks
 // (lane l: block l & 7, 4 rows); the bit planes are then packed per block.
 // ---------------------------------------------------------------------------
+// The per-warp encode core, shared by the standalone encode and the fused last-step kernel: the
+// lane holds 4 rows (r0 + 4u, r = yi + 4 zi) of block ib (v), `live` says whether that block is
+// written, bit i of live_mask whether block i is.  rec0 = the first block's record (32-bit words),
+// cw = this warp's 8 x CODE_LD code scratch.  Returns true if a live value was rejected.
 template <bool TWO, int QT>
-__global__ void __launch_bounds__(CODEC_WARPS * 32)
-bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int nbx, int nby,
-                 int64_t pitch, int64_t pstride, int q_rt, int *err) {
+__device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, uint32_t live_mask, uint32_t *rec0,
+                                               int q_rt, uint32_t (*cw)[CODE_LD], int lane) {
     const int q = QT ? QT : q_rt;
-    __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const LineTask t = line_task(nbx);
-    if (t.by >= nby) return;
-    // ---- load straight into the statistics layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12
-    //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging)
     const int ib = lane & 7, r0 = lane >> 3;
-    const bool live = ib < t.nb;
-    const float *sbase = src + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
-    float4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 4 * u;  // r = yi + 4 zi
-        v[u] = live ? __ldcs(reinterpret_cast<const float4 *>(sbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
     float mn = v[0].x, mx = v[0].x;
     bool nan = false;
 #pragma unroll
@@ -195,17 +183,14 @@ bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int n
     auto code = [&](float x) -> uint32_t {
         return small ? 0u : min(cmax, __float2uint_rd(__fmul_rn(__fsub_rn(x, mn), scale)));
     };
-    uint32_t(*cw)[CODE_LD] = codes[warp];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int r = r0 + 4 * u;  // r = yi + 4 zi, so j = xi + 4 r
-        *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) =
-            make_uint4(code(v[u].x), code(v[u].y), code(v[u].z), code(v[u].w));
+        *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) = make_uint4(code(v[u].x), code(v[u].y), code(v[u].z), code(v[u].w));
     }
     __syncwarp();
     // ---- bit planes: lane m of the transpose owns plane (m & 15), half (m >> 4)
     const int recw = 2 * (q + 1);
-    uint32_t *rec0 = reinterpret_cast<uint32_t *>(dst) + ((int64_t)(t.bz * nby + t.by) * nbx + t.b0) * recw;
     const Xpose X(lane);
     const int b = lane & 15, half = lane >> 4;
     const int wi0 = b < q ? 2 + 2 * (q - 1 - b) + half : -1;
@@ -214,7 +199,7 @@ bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int n
     for (int i = 0; i < 8; ++i) {  // unconditional (convergent shuffles); stores only for live blocks
         const uint32_t c_lo = cw[i][lane], c_hi = cw[i][lane + 32];
         uint32_t *rec = rec0 + i * recw;
-        const bool st = i < t.nb;
+        const bool st = (live_mask >> i) & 1u;
         const uint32_t T0 = X((c_lo & 0xFFFFu) | (c_hi << 16));
         if (st && wi0 >= 0) rec[wi0] = T0;
         if (TWO) {
@@ -224,6 +209,45 @@ bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int n
     }
     // block headers straight from the statistics lanes (lane l < 8 holds block l's mn/mx)
     if (lane < 8 && live) *reinterpret_cast<uint2 *>(rec0 + lane * recw) = make_uint2(__float_as_uint(mn), __float_as_uint(mx));
+    __syncwarp();
+    return bad;
+}
+
+// edge: 0 = every block; 1 = only the x-boundary blocks bx = 0 / nbx-1 (grid.x = 2); 2 = only the
+// y-boundary block rows by = 0 / nby-1 (grid.y = 1, warps 0/1).  Edge modes encode the halo blocks
+// the fused last-step kernel does not produce; they hold the fixed Dirichlet values, identical in
+// every time level, so any array of the working set is a valid source.
+template <bool TWO, int QT>
+__global__ void __launch_bounds__(CODEC_WARPS * 32)
+bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int nbx, int nby,
+                 int64_t pitch, int64_t pstride, int q_rt, int *err, int edge) {
+    const int q = QT ? QT : q_rt;
+    __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    LineTask t = line_task(nbx);
+    if (edge == 1) {
+        t.b0 = blockIdx.x ? nbx - 1 : 0;
+        t.nb = 1;
+    } else if (edge == 2) {
+        if (warp >= 2) return;
+        t.by = warp ? nby - 1 : 0;
+    }
+    if (t.by >= nby) return;
+    // ---- load straight into the statistics layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12
+    //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging)
+    const int ib = lane & 7, r0 = lane >> 3;
+    const bool live = ib < t.nb;
+    const float *sbase = src + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 4 * u;  // r = yi + 4 zi
+        v[u] = live ? __ldcs(reinterpret_cast<const float4 *>(sbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int recw = 2 * (q + 1);
+    uint32_t *rec0 = reinterpret_cast<uint32_t *>(dst) + ((int64_t)(t.bz * nby + t.by) * nbx + t.b0) * recw;
+    const bool bad = bq_encode_core<TWO, QT>(v, live, (1u << t.nb) - 1u, rec0, q, codes[warp], lane);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1);
 }
 
@@ -261,19 +285,31 @@ __global__ void id_encode_kernel(const float *__restrict__ src, float4 *__restri
 // queue indexed at compile time (the plane loop is unrolled by 9), x/y
 // neighbours come from the ring with 64-bit shared loads.
 // ---------------------------------------------------------------------------
-constexpr int S2_TX = 64, S2_TY = 16, S2_THREADS = 256;
-constexpr int S2_PW = S2_TX + 2 * R, S2_PH = S2_TY + 2 * R;  // 72 x 24 p_curr box
-constexpr int S2_NS = 9;                                       // p_curr ring slots
-constexpr int S2_NB = 3;                                       // p_prev / v stages
-constexpr int S2_D = 2;                                        // prefetch distance (planes)
-constexpr uint32_t S2_PBYTES = S2_PW * S2_PH * 4, S2_TBYTES = S2_TX * S2_TY * 4;
-struct S2Smem {
-    float p[S2_NS][S2_PH][S2_PW];
-    float pp[S2_NB][S2_TY][S2_TX];
-    float v[S2_NB][S2_TY][S2_TX];
-    unsigned long long bar[S2_NB + 1];
+// TY = tile rows (16: 256 threads, 2 CTAs per SM).  The p_curr ring has 7 slots: at plane z it holds
+// the x/y-neighbour plane z, the queue-feed plane z+4 and the two planes in flight (z+5, z+6).
+template <int TY>
+struct S2T {
+    static constexpr int TX = 64, THREADS = 16 * TY, CTAS = TY == 16 ? 2 : 1;
+    static constexpr int PW = TX + 2 * R, PH = TY + 2 * R;  // p_curr box with the star halo
+    static constexpr int NS = 7, NB = 3, D = 2;             // ring slots, p_prev/v stages, prefetch distance
+    static constexpr uint32_t PBYTES = PW * PH * 4, TBYTES = TX * TY * 4;
 };
-constexpr size_t S2_SMEM = sizeof(S2Smem);
+// ENC selects the stencil variant: 0 = plain step; otherwise the last step of a sweep that also
+// encodes its owned slabs, with one BlockQuant encoder compiled in (q = 15 specialised, generic
+// one-word q <= 16, generic two-word q > 16), keeping the kernel's instruction footprint small
+enum { ENC_NONE = 0, ENC_Q15 = 1, ENC_ONE = 2, ENC_TWO = 3 };
+
+template <int TY, int ENC>
+struct S2Smem {
+    float p[7][TY + 2 * R][64 + 2 * R];
+    float pp[3][TY][64];
+    float v[3][TY][64];
+    // ENC: the 4-plane slab being completed, [prev/curr][plane][row][col]; the encode phase reuses it
+    // as the warps' code scratch
+    float stage[ENC ? 2 : 1][ENC ? 4 : 1][ENC ? TY : 1][ENC ? 64 : 4];
+    unsigned long long bar[4];
+};
+constexpr int S2_TX = 64, S2_NS = 7, S2_NB = 3, S2_D = 2;
 
 // coefficients of d2/dx2, order 8 (Q1): 8/5, -1/5, 8/315, -1/560
 #define C1 1.6f
@@ -316,22 +352,31 @@ struct StepArgs {
     int nx, ny, z_lo, z_hi, zchunk, gx;
     int64_t pitch, pstride;
     float dt;
+    // ENC only: records of the owned slabs [z_lo, z_hi) of (prev = level k-1, curr = level k)
+    uint32_t *out[2];
+    int nbx, nby, q;
+    int *err;
 };
 
+template <int TY, int ENC>
+__device__ __noinline__ void s2_encode_slab(S2Smem<TY, ENC> &S, const StepArgs &a, int x0, int y0, int zslab);
+
 // one plane of the march; OFF = (z - zs) mod 9 is a compile-time register-queue rotation
-template <int OFF>
-__device__ __forceinline__ bool s2_plane(S2Smem &S, const CUtensorMap *mP, const CUtensorMap *mPP,
+template <int OFF, int TY, int ENC>
+__device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *mP, const CUtensorMap *mPP,
                                          const CUtensorMap *mV, const StepArgs &a, int z, int zs, int ze,
-                                         int x0, int y0, float (&q)[S2_NS][4], uint32_t &ph, bool okr0,
+                                         int x0, int y0, float (&q)[9][4], uint32_t &ph, bool okr0,
                                          bool okr1, int64_t g0) {
     if (z >= ze) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // every thread is done with plane z-1: its ring slots may be refilled
+    // ring slot of plane P is (P - zs + 4) mod 7
+    const int rel = z - zs;
     if (tid == 0 && z + S2_D < ze) {
-        constexpr int ps = (OFF + 1) % S2_NS;        // slot of plane z+D+4 (== slot of plane z-3)
+        const int ps = (rel + 4 + S2_D + R) % S2_NS;  // slot of plane z+D+4 (previously plane z-1)
         constexpr int st = (OFF + S2_D) % S2_NB;     // stage of plane z+D
         unsigned long long *bar = &S.bar[st];
-        mbar_expect_tx(bar, S2_PBYTES + 2 * S2_TBYTES);
+        mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
         tma_load_3d(&S.p[ps][0][0], mP, XOFF + x0, y0, z + S2_D + R, bar);
         tma_load_3d(&S.pp[st][0][0], mPP, XOFF + R + x0, R + y0, z + S2_D, bar);
         tma_load_3d(&S.v[st][0][0], mV, XOFF + R + x0, R + y0, z + S2_D, bar);
@@ -339,7 +384,7 @@ __device__ __forceinline__ bool s2_plane(S2Smem &S, const CUtensorMap *mP, const
     constexpr int st = OFF % S2_NB;
     mbar_wait(&S.bar[st], (ph >> st) & 1u);
     ph ^= 1u << st;
-    constexpr int sz = (OFF + 4) % S2_NS, sz4 = (OFF + 8) % S2_NS;
+    const int sz = (rel + 4) % S2_NS, sz4 = (rel + 4 + R) % S2_NS;
     const int cx = 2 * lane, cy = 2 * warp;
     // feed the queue with plane z+4 (own cells)
     {
@@ -350,7 +395,7 @@ __device__ __forceinline__ bool s2_plane(S2Smem &S, const CUtensorMap *mP, const
         q[(OFF + 8) % 9][2] = a1.x;
         q[(OFF + 8) % 9][3] = a1.y;
     }
-    const float(*P)[S2_PW] = S.p[sz];
+    const float(*P)[S2T<TY>::PW] = S.p[sz];
     // y neighbours: rows cy..cy+3 and cy+6..cy+9 of the box at columns cx+4, cx+5
     float2 yr[10];
 #pragma unroll
@@ -402,19 +447,81 @@ __device__ __forceinline__ bool s2_plane(S2Smem &S, const CUtensorMap *mP, const
             out[ci] = __fmaf_rn(__fmul_rn(vd, vd), lap, __fsub_rn(f2, pv));
         }
     }
-    float *dst = a.pprev + (int64_t)z * a.pstride + g0;
-    if (okr0) __stcs(reinterpret_cast<float2 *>(dst), make_float2(out[0], out[1]));
-    if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), make_float2(out[2], out[3]));
+    if (!ENC) {
+        float *dst = a.pprev + (int64_t)z * a.pstride + g0;
+        if (okr0) __stcs(reinterpret_cast<float2 *>(dst), make_float2(out[0], out[1]));
+        if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), make_float2(out[2], out[3]));
+    } else {
+        // last step: level k is not written back; (level k-1, level k) of the own cells go to the
+        // slab staging, and a completed 4-plane slab is encoded straight into the records
+        const int sl = (z - zs) & 3;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            *reinterpret_cast<float2 *>(&S.stage[0][sl][cy + r][cx]) =
+                make_float2(q[(OFF + 4) % 9][2 * r], q[(OFF + 4) % 9][2 * r + 1]);
+            *reinterpret_cast<float2 *>(&S.stage[1][sl][cy + r][cx]) = make_float2(out[2 * r], out[2 * r + 1]);
+        }
+        if (sl == 3) s2_encode_slab<TY, ENC>(S, a, x0, y0, z - 3);
+    }
     return true;
 }
 
-__global__ void __launch_bounds__(S2_THREADS, 2)
+// encode the staged 4-plane slab (planes zslab..zslab+3) of both arrays: 2 arrays x TY/4 block rows x
+// 2 groups of 8 x-adjacent blocks; every warp first loads the rows of its tasks, then (the staging is
+// reused as code scratch) encodes them with the standalone encoder's core
+template <int TY, int ENC>
+__device__ __noinline__ void s2_encode_slab(S2Smem<TY, ENC> &S, const StepArgs &a, int x0, int y0, int zslab) {
+    if constexpr (ENC) {
+        constexpr int NW = S2T<TY>::THREADS / 32, NT = 2 * (TY / 4) * 2, TPW = NT / NW;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int ib = lane & 7, r0 = lane >> 3;
+        __syncthreads();  // the whole slab is staged
+        float4 v[TPW][4];
+        bool live[TPW];
+        int arr[TPW], byl[TPW], bxl0[TPW];
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+            const int tk = warp + j * NW;
+            arr[j] = tk / (2 * (TY / 4));
+            byl[j] = (tk >> 1) % (TY / 4);
+            bxl0[j] = 8 * (tk & 1);
+            const int bxl = bxl0[j] + ib;
+            live[j] = x0 + 4 * bxl < a.nx && y0 + 4 * byl[j] < a.ny;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = r0 + 4 * u;  // yi = r & 3, zi = r >> 2
+                v[j][u] = *reinterpret_cast<const float4 *>(&S.stage[arr[j]][r >> 2][4 * byl[j] + (r & 3)][4 * bxl]);
+            }
+        }
+        __syncthreads();  // staging now free: reuse it as per-warp code scratch
+        uint32_t(*cw)[CODE_LD] = reinterpret_cast<uint32_t(*)[CODE_LD]>(&S.stage[0][0][0][0]) + warp * 8;
+        const int recw = 2 * (a.q + 1);
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+            const uint32_t mask = __ballot_sync(0xffffffffu, live[j] && r0 == 0) & 0xFFu;
+            const int bz = (zslab - a.z_lo) >> 2;
+            const int by = 1 + (y0 >> 2) + byl[j], bx = 1 + (x0 >> 2) + bxl0[j];
+            uint32_t *rec0 = a.out[arr[j]] + ((int64_t)(bz * a.nby + by) * a.nbx + bx) * recw;
+            if constexpr (ENC == ENC_Q15)
+                bad |= bq_encode_core<false, 15>(v[j], live[j], mask, rec0, 15, cw, lane);
+            else if constexpr (ENC == ENC_TWO)
+                bad |= bq_encode_core<true, 0>(v[j], live[j], mask, rec0, a.q, cw, lane);
+            else
+                bad |= bq_encode_core<false, 0>(v[j], live[j], mask, rec0, a.q, cw, lane);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1);
+    }
+}
+
+template <int TY, int ENC>
+__global__ void __launch_bounds__(S2T<TY>::THREADS, S2T<TY>::CTAS)
 stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mPP,
                         const __grid_constant__ CUtensorMap mV, const StepArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    S2Smem &S = *reinterpret_cast<S2Smem *>(smem_raw);
+    S2Smem<TY, ENC> &S = *reinterpret_cast<S2Smem<TY, ENC> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int x0 = blockIdx.x * S2_TX, y0 = blockIdx.y * S2_TY;
+    const int x0 = blockIdx.x * S2_TX, y0 = blockIdx.y * TY;
     const int zs = a.z_lo + blockIdx.z * a.zchunk;
     const int ze = min(a.z_hi, zs + a.zchunk);
     if (zs >= ze) return;
@@ -432,20 +539,20 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
         // prologue: p_curr planes zs..zs+3 (x/y neighbours of the first 4 planes), then the
         // first D stages (plane z+4 of p_curr, plane z of p_prev and v)
         unsigned long long *pro = &S.bar[S2_NB];
-        mbar_expect_tx(pro, 4 * S2_PBYTES);
+        mbar_expect_tx(pro, 4 * S2T<TY>::PBYTES);
         for (int i = 0; i < 4; ++i) tma_load_3d(&S.p[(4 + i) % S2_NS][0][0], &mP, XOFF + x0, y0, zs + i, pro);
         for (int j = 0; j < S2_D; ++j) {
             const int z = zs + j;
             if (z >= ze) break;
             unsigned long long *bar = &S.bar[j % S2_NB];
-            mbar_expect_tx(bar, S2_PBYTES + 2 * S2_TBYTES);
-            tma_load_3d(&S.p[(j + 8) % S2_NS][0][0], &mP, XOFF + x0, y0, z + R, bar);
+            mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
+            tma_load_3d(&S.p[(j + 4 + R) % S2_NS][0][0], &mP, XOFF + x0, y0, z + R, bar);
             tma_load_3d(&S.pp[j % S2_NB][0][0], &mPP, XOFF + R + x0, R + y0, z, bar);
             tma_load_3d(&S.v[j % S2_NB][0][0], &mV, XOFF + R + x0, R + y0, z, bar);
         }
     }
     // register queue: planes zs-4 .. zs+3 of the own 2x2 cells (index m <-> plane zs-4+m)
-    float q[S2_NS][4];
+    float q[9][4];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         const float *src = a.pcurr + (int64_t)(zs - R + m) * a.pstride + g0;
@@ -458,15 +565,15 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
     mbar_wait(&S.bar[S2_NB], 0);
     uint32_t ph = 0;
     for (int zb = zs; zb < ze; zb += 9) {
-        if (!s2_plane<0>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<1>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<2>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<3>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<4>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<5>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<6>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<7>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<8>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<0, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<1, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<2, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<3, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<4, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<5, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<6, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<7, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<8, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
     }
 }
 
@@ -863,7 +970,7 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
     const int nl = (int)nlines_of(ax);
     const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(planes / 4));
     uint8_t *d8 = static_cast<uint8_t *>(dst);
-#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err)
+#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 0)
     switch (q) {
     case 7: ENC(false, 7); break;
     case 11: ENC(false, 11); break;
@@ -907,18 +1014,20 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t pitch, int64_t a
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
-                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st) {
+template <int TY, int ENC>
+static cudaError_t launch_stencil(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay,
+                                  int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, StepArgs a,
+                                  cudaStream_t st) {
     if (z_hi <= z_lo) return cudaSuccess;
+    const size_t smem = sizeof(S2Smem<TY, ENC>);
     // per device (the attribute is per function and device); idempotent, so racing threads are harmless
-    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)S2_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel<TY, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mP, mPP, mV;
-    if (!make_map(&mP, pcurr, pitch, ay, planes, S2_PW, S2_PH) || !make_map(&mPP, pprev, pitch, ay, planes, S2_TX, S2_TY) ||
-        !make_map(&mV, vel, pitch, ay, planes, S2_TX, S2_TY))
+    if (!make_map(&mP, pcurr, pitch, ay, planes, S2T<TY>::PW, S2T<TY>::PH) ||
+        !make_map(&mPP, pprev, pitch, ay, planes, S2_TX, TY) || !make_map(&mV, vel, pitch, ay, planes, S2_TX, TY))
         return cudaErrorInvalidValue;
-    StepArgs a;
     a.pprev = pprev;
     a.pcurr = pcurr;
     a.nx = (int)(ax - 2 * R);
@@ -928,14 +1037,15 @@ cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int6
     a.pitch = pitch;
     a.pstride = ay * pitch;
     a.dt = dt;
-    const int gx = (a.nx + S2_TX - 1) / S2_TX, gy = (a.ny + S2_TY - 1) / S2_TY;
+    const int gx = (a.nx + S2_TX - 1) / S2_TX, gy = (a.ny + TY - 1) / TY;
     a.gx = gx;
-    // split z so the grid is close to a whole number of waves (2 CTAs per SM resident)
-    const int Z = (int)(z_hi - z_lo), tiles = gx * gy, res = 148 * 2;
+    // split z so the grid is close to a whole number of waves; the encoding variant splits on 4-plane slabs
+    const int Z = (int)(z_hi - z_lo), tiles = gx * gy, res = 148 * S2T<TY>::CTAS;
+    const int unit = ENC ? 4 : 1;
     int best = 1;
     double best_eff = 0;
     for (int nzc = 1; nzc <= 16; ++nzc) {
-        const int chunk = (Z + nzc - 1) / nzc;
+        const int chunk = ((Z + nzc - 1) / nzc + unit - 1) / unit * unit;
         if (nzc > 1 && chunk < 24) break;
         const int items = tiles * ((Z + chunk - 1) / chunk);
         const double waves = (double)items / res;
@@ -945,10 +1055,55 @@ cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int6
             best = nzc;
         }
     }
-    a.zchunk = (Z + best - 1) / best;
+    a.zchunk = ((Z + best - 1) / best + unit - 1) / unit * unit;
     const int nzc = (Z + a.zchunk - 1) / a.zchunk;
     dim3 grid(gx, gy, nzc);
-    stencil_step_tma_kernel<<<grid, S2_THREADS, S2_SMEM, st>>>(mP, mPP, mV, a);
+    stencil_step_tma_kernel<TY, ENC><<<grid, S2T<TY>::THREADS, smem, st>>>(mP, mPP, mV, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
+                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st) {
+    StepArgs a{};
+    return launch_stencil<16, ENC_NONE>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+}
+
+cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,
+                               int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
+                               void *out_prev, void *out_curr, int *err, cudaStream_t st) {
+    if ((z_lo | z_hi) & 3) return cudaErrorInvalidValue;  // whole 4-plane slabs
+    StepArgs a{};
+    a.out[0] = static_cast<uint32_t *>(out_prev);
+    a.out[1] = static_cast<uint32_t *>(out_curr);
+    a.nbx = (int)(ax / 4);
+    a.nby = (int)(ay / 4);
+    a.q = q;
+    a.err = err;
+    float *pp = const_cast<float *>(pprev);
+    cudaError_t e = q == 15  ? launch_stencil<16, ENC_Q15>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st)
+                    : q > 16 ? launch_stencil<16, ENC_TWO>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st)
+                             : launch_stencil<16, ENC_ONE>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+    if (e != cudaSuccess) return e;
+    // the x/y halo blocks of the owned slabs (constant Dirichlet values, same in both arrays) are not
+    // produced by the fused kernel: encode them with the standalone encoder's edge modes
+    const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+    const int nl = (int)nlines_of(ax);
+    const int64_t pstride = ay * pitch;
+    const int slabs = (int)((z_hi - z_lo) / 4);
+    const float *src = pcurr + z_lo * pstride;
+    for (int j = 0; j < 2; ++j) {
+        uint8_t *d8 = static_cast<uint8_t *>(j ? out_curr : out_prev);
+        const dim3 gx2(2, (unsigned)((nby + 7) / 8), (unsigned)slabs), gy2((unsigned)nl, 1, (unsigned)slabs);
+#define EDGE(TWO, QT)                                                                                        \
+    do {                                                                                                     \
+        bq_encode_kernel<TWO, QT><<<gx2, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 1); \
+        bq_encode_kernel<TWO, QT><<<gy2, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 2); \
+    } while (0)
+        if (q == 15) EDGE(false, 15);
+        else if (q > 16) EDGE(true, 0);
+        else EDGE(false, 0);
+#undef EDGE
+    }
     return cudaGetLastError();
 }
 

@@ -45,6 +45,10 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
                           int codec, int q, int *err, cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
+// last step fused with the BlockQuant encode of the owned slabs [z_lo, z_hi) (device store)
+cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,
+                               int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
+                               void *out_prev, void *out_curr, int *err, cudaStream_t st);
 
 void set_error(const std::string &msg);
 

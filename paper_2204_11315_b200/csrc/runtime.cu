@@ -165,6 +165,29 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
     return OOCS_OK;
 }
 
+// device store + BlockQuant, opted in: the last step of a chunk is fused with the encode
+static bool fuse_last_step(const Plan *p) {
+    const Geometry &g = p->geo;
+    return !g.host_store && g.codec == OOCS_CODEC_BLOCKQUANT && (g.cfg.flags & OOCS_FLAG_FUSE_ENCODE);
+}
+
+static oocs_status k_step_encode(Plan *p, const float *v, const float *pp, const float *pc, int64_t zlo, int64_t zhi,
+                                 void *out_prev, void *out_curr, cudaStream_t st, oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 1);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_step_encode(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi, p->geo.cfg.dt,
+                          p->geo.q, out_prev, out_curr, p->d_err, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[1]++;
+        const uint64_t cells = (uint64_t)(zhi - zlo) * p->geo.nx * p->geo.ny;
+        stats->cell_updates_computed += cells;
+        // read p_curr, p_prev, v (12 B); write two compressed values (2 r/8 B)
+        stats->alg_bytes[1] += cells * 12 + (uint64_t)(zhi - zlo) * 2 * pb(p);
+    }
+    return OOCS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // plan create / destroy
 // ---------------------------------------------------------------------------
@@ -483,12 +506,23 @@ static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats 
             const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
             const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
             const int up = upd_array(sidx), other = 3 - up;
+            if (fuse_last_step(p) && sidx == g.k) {
+                // the last step and the encode of the owned slabs in one kernel: level k is never
+                // written back, (level k-1, level k) go straight to S_{t+1}'s records
+                void *out_prev = p->dstore[p->cur ^ 1][1] + hoff(p, b.own_lo);
+                void *out_curr = p->dstore[p->cur ^ 1][2] + hoff(p, b.own_lo);
+                oocs_status r = k_step_encode(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
+                                              hi - b.ext_lo, out_prev, out_curr, st, stats);
+                if (r) return r;
+                break;
+            }
             oocs_status r = k_step(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo, st,
                                    stats);
             if (r) return r;
             break;
         }
         case OOCS_OP_ENCODE: {
+            if (fuse_last_step(p)) break;  // done by the fused last step
             // after k steps: level t0+k in array upd(k), level t0+k-1 in the other
             const int curr = upd_array(g.k), prev = 3 - curr;
             const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;

@@ -337,3 +337,23 @@ def test_degenerate_cases():
     _, pc = oracle.incore(vel, p0.copy(), p0.copy(), synth.dt_for(), 4)
     assert _rel_err(a1.store(2, 0, 40), pc.astype(np.float64)) <= 4e-6
     a1.close()
+
+
+@pytest.mark.parametrize("rate", [8, 12, 16, 24])
+@pytest.mark.parametrize("nx,ny,nz,n,k", [(40, 32, 64, 4, 2), (72, 44, 48, 3, 1), (132, 100, 96, 2, 3)])
+def test_fused_last_step_encode_bitwise(rate, nx, ny, nz, n, k):
+    """Device store: the last step fused with the encode (incl. the halo-block edge encodes) writes the
+    same S_{t+1} bytes as the separate step + encode kernels."""
+    vel, p0 = synth.fields(nx, ny, nz)
+    az = nz + 2 * R
+    outs = []
+    for fusion in (False, True):
+        c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k,
+                             rate_bits=rate, mode="swb", store="device", fusion=fusion)
+        pl = oocs.Plan(c)
+        load_fields(pl, vel, p0)
+        pl.run(2 * k)
+        outs.append([pl.read_raw(a, 0, az) for a in (1, 2)])
+        pl.close()
+    for a in range(2):
+        assert np.array_equal(outs[0][a], outs[1][a]), (a, np.flatnonzero(outs[0][a] != outs[1][a])[:8])
