@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--fuse-encode", action="store_true", help="fuse each chunk's last step with its encode "
                     "(device store, BlockQuant; OOCS_FLAG_FUSE_ENCODE)")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
-    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp"],
+    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp", "trunc16"],
                     help="fixed-rate codec of the compressed state (ZFP = NEXT-1)")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
                     help="stream/event schedule of the host-store pipeline (e2e)")
@@ -192,9 +192,13 @@ def agg(stats_list):
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def cpu_oracle_sample(nx, ny, k, rate, device=None):
+ORACLE_CODEC = {"blockquant": (1, lambda r: r - 1), "zfp": (2, lambda r: r), "trunc16": (3, lambda r: 0)}
+CODEC_NAME = {"blockquant": "BlockQuant", "zfp": "ZFP", "trunc16": "Truncate-16 (bf16)"}
+
+
+def cpu_oracle_sample(nx, ny, k, rate, device=None, codec="blockquant"):
     """Bounded sample of the workload through the CPU oracle: a nx*ny*256 slab (two of c2's
-    128-plane chunks, interior-size trapezoids), one sweep of k steps, BlockQuant rate `rate`."""
+    128-plane chunks, interior-size trapezoids), one sweep of k steps, the same codec and rate."""
     import oracle
     import synth
 
@@ -204,19 +208,20 @@ def cpu_oracle_sample(nx, ny, k, rate, device=None):
         v, p = v.cpu().numpy(), p.cpu().numpy()
     else:
         v, p = synth.fields(nx, ny, nz)
-    q = rate - 1
-    S = [oracle.encode_planes(a, 1, q) for a in (v, p, p)]
+    cid, qf = ORACLE_CODEC[codec]
+    q = qf(rate)
+    S = [oracle.encode_planes(a, cid, q) for a in (v, p, p)]
     ax, ay = nx + 2 * R, ny + 2 * R
     dt = synth.dt_for()
 
     def one():
         Sp, Sc = S[1].copy(), S[2].copy()
         t0 = time.perf_counter()
-        oracle.pipeline(ax, ay, nz, 2, k, dt, k, 1, q, S[0], Sp, Sc)
+        oracle.pipeline(ax, ay, nz, 2, k, dt, k, cid, q, S[0], Sp, Sc)
         return time.perf_counter() - t0
 
     cells = nx * ny * nz * k
-    sample = f"CPU oracle pipeline on a {nx}x{ny}x{nz} slab (2 chunks of 128 planes), 1 sweep of k={k} steps, rate {rate}"
+    sample = f"CPU oracle pipeline on a {nx}x{ny}x{nz} slab (2 chunks of 128 planes), 1 sweep of k={k} steps, {CODEC_NAME[codec]} rate {rate}"
     return one, cells, sample
 
 
@@ -232,12 +237,14 @@ def main():
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     nx, ny, nzr, nbr, k, T, rate = WORKLOADS[args.workload]
+    if args.codec == "trunc16":
+        rate = 16  # bfloat16
     import torch
 
     nz = nzr * world
     nblocks = nbr * world
     workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps, "
-                f"temporal depth k={k}, {'ZFP' if args.codec == 'zfp' else 'BlockQuant'} rate {rate} bits/value, "
+                f"temporal depth k={k}, {CODEC_NAME[args.codec]} rate {rate} bits/value, "
                 f"single working buffer")
     config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
               "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
@@ -249,7 +256,8 @@ def main():
         if rank != 0:
             return
         one, cells, sample = cpu_oracle_sample(nx, ny, k, rate,
-                                               device="cuda" if torch.cuda.is_available() else None)
+                                               device="cuda" if torch.cuda.is_available() else None,
+                                               codec=args.codec)
         for _ in range(args.warmup):
             one()
         secs = sum(one() for _ in range(args.steps))
@@ -419,7 +427,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        one, cells, sample = cpu_oracle_sample(nx, ny, k, rate, device=f"cuda:{local}")
+        one, cells, sample = cpu_oracle_sample(nx, ny, k, rate, device=f"cuda:{local}", codec=args.codec)
         secs = one()
         cpu = {"value": cells / secs / 1e9, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
                "sample": sample, "seconds": secs}

@@ -70,7 +70,10 @@ typedef enum {
 typedef enum {
     OOCS_CODEC_IDENTITY = 0,   /* raw fp32 (rate 32) */
     OOCS_CODEC_BLOCKQUANT = 1, /* fixed-rate 4x4x4 block quantiser, rate_bits in [2, 24] */
-    OOCS_CODEC_ZFP = 2         /* ZFP fixed-rate (cuZFP's algorithm), rate_bits in [1, 32]; record = 8*rate B */
+    OOCS_CODEC_ZFP = 2,        /* ZFP fixed-rate (cuZFP's algorithm), rate_bits in [1, 32]; record = 8*rate B */
+    OOCS_CODEC_TRUNC16 = 3     /* Truncate-16: fp32 -> bfloat16, round to nearest even, NaN -> 0x7FC0;
+                                * rate_bits must be 16; raw bf16 planes (ax*ay*2 B per plane, x fastest); never
+                                * reports OOCS_ERR_DATA (Inf stays Inf, finite values above the bf16 range round to Inf) */
 } oocs_codec;
 
 /* Pipeline architectures of the paper (Fig. 6 `fig:3ver`, Fig. 7 `fig:swb`). */
@@ -105,6 +108,20 @@ typedef enum {
  * 35% fewer HBM bytes than step + encode but is issue-bound and measures ~1.5%
  * slower on B200.  Ignored by other modes. */
 #define OOCS_FLAG_FUSE_ENCODE 4u
+/* Record a CUDA-event span around every work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) of a
+ * run; read it back with oocs_timeline (the analog of the paper's pipeline figures fig:pipe1 /
+ * fig:newbot).  Costs two event records per op. */
+#define OOCS_FLAG_TIMELINE 8u
+/* Executors.  By default a host dispatcher issues the schedule's work ops by dependency: kernels on
+ * their lane's kernel stream with device-side waits, copies only once their dependencies have completed,
+ * on one stream per direction -- so no copy stream ever holds a pending cross-stream wait (a copy channel
+ * blocked on a wait was measured, OOCS_FLAG_TIMELINE, to be re-examined only when the copy engine's
+ * current DMA ends: DESIGN.md §8).  These flags replay the schedule onto streams instead:
+ * LANE_SINGLE_STREAM = one CUDA stream per lane, the literal mapping of Alg. 1's three streams;
+ * LANE_SPLIT_STREAMS = a copy and a kernel stream per lane, joined by an event at every switch.  All
+ * three execute the same dependencies and produce the same bytes. */
+#define OOCS_FLAG_LANE_SINGLE_STREAM 16u
+#define OOCS_FLAG_LANE_SPLIT_STREAMS 32u
 
 typedef struct {
     uint32_t struct_size;     /* sizeof(oocs_config): ABI versioning */
@@ -173,6 +190,21 @@ typedef struct {
     int32_t pad;
     int64_t ev_g;  /* WAIT/RECORD: block counter of the event */
 } oocs_op;
+
+/* One recorded op of the last oocs_run under OOCS_FLAG_TIMELINE: when its lane reached it (start) and
+ * finished it (end), in ms from the run's first event.  A copy's start is when its stream issued it; it
+ * may then queue behind another lane's copy on the same DMA engine. */
+typedef struct {
+    int32_t kind;  /* oocs_op_kind (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) */
+    int32_t lane;
+    int64_t g;     /* global block counter */
+    int32_t block;
+    int32_t sweep;
+    int32_t arg;   /* STEP: step index s */
+    int32_t pad;
+    double start_ms, end_ms;
+    double host_ms; /* host wall clock when the op was enqueued, ms from the run's start (enqueue lag) */
+} oocs_span;
 
 typedef enum {
     OOCS_OP_H2D = 0, OOCS_OP_CARRY = 1, OOCS_OP_DECODE = 2, OOCS_OP_STEP = 3,
@@ -271,6 +303,11 @@ oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src
  * Errors: OOCS_ERR_CONFIG (steps), OOCS_ERR_DATA (encoder rejected a value;
  * state undefined), OOCS_ERR_CUDA, OOCS_ERR_EXCHANGE, OOCS_ERR_STATE. */
 oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out);
+
+/* Spans of the last oocs_run made with OOCS_FLAG_TIMELINE, in schedule order.  Copies min(cap, n)
+ * spans into out (out may be NULL to query n); *n_spans = n (0 if the flag was not set).
+ * Errors: OOCS_ERR_CONFIG for NULL plan / n_spans, OOCS_ERR_STATE for a poisoned plan. */
+oocs_status oocs_timeline(const oocs_plan *plan, oocs_span *out, int64_t cap, int64_t *n_spans);
 
 /* ---- hot-path kernels, callable on caller device memory --------------- */
 /* Working-buffer layout for these calls: planes x ay rows x `pitch` floats,

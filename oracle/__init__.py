@@ -24,6 +24,7 @@ R = 4  # stencil radius (P:L190 HALO=4, P:L212 25-point)
 CODEC_IDENTITY = 0
 CODEC_BLOCKQUANT = 1
 CODEC_ZFP = 2  # the codec parameter is the rate (bits/value) for ZFP, q = rate - 1 for BlockQuant
+CODEC_TRUNC16 = 3  # fp32 -> bfloat16 RNE; the codec parameter is unused
 
 
 def build(force: bool = False) -> str:
@@ -71,6 +72,10 @@ def lib():
         L.oracle_zfp_int2uint.restype = ctypes.c_uint32
         L.oracle_zfp_uint2int.argtypes = [ctypes.c_uint32]
         L.oracle_zfp_uint2int.restype = ctypes.c_int32
+        L.oracle_tr16_encode.argtypes = [f32]
+        L.oracle_tr16_encode.restype = ctypes.c_uint16
+        L.oracle_tr16_decode.argtypes = [ctypes.c_uint16]
+        L.oracle_tr16_decode.restype = f32
         _lib = L
     return _lib
 
@@ -196,3 +201,12 @@ def zfp_int2uint(x: int) -> int:
 
 def zfp_uint2int(u: int) -> int:
     return int(lib().oracle_zfp_uint2int(u))
+
+
+# ---- Truncate-16 -----------------------------------------------------------------
+def tr16_encode(x: float) -> int:
+    return int(lib().oracle_tr16_encode(float(np.float32(x))))
+
+
+def tr16_decode(h: int) -> float:
+    return float(lib().oracle_tr16_decode(h))

@@ -25,7 +25,9 @@
  *                            S:L242-244, adapted to fp32 -- DESIGN.md §3 Q11-Q14)
  *   oracle_encode_planes / oracle_decode_planes
  *                            array-level codec over whole 4-plane slabs
- *                            (identity or BlockQuant), slab-major block order
+ *                            (identity, BlockQuant, ZFP, Truncate-16), slab-major block order
+ *   oracle_tr16_encode / oracle_tr16_decode
+ *                            Truncate-16: fp32 -> bfloat16 round-to-nearest-even
  *   oracle_plan              z-chunk decomposition with temporal-blocking halo
  *                            and region-sharing overlap (§3.1)
  *   oracle_pipeline          the out-of-core method, step by step in the
@@ -209,12 +211,35 @@ void oracle_bq_decode_block(const uint8_t *rec, int q, float *x) {
 }
 
 int oracle_zfp_encode_planes(int64_t ax, int64_t ay, int64_t planes, const float *src, int rate, uint8_t *dst);
+
+/* Truncate-16 (SURVEY.md §8(b) codec enum, §8(c) C-3 "Truncate-16: fp32 -> bf16 RNE (the upper 16 bits
+ * after RNE rounding; NaN -> quiet NaN)").  Written out on the bit pattern: bfloat16 keeps the sign,
+ * the 8 exponent bits and the top 7 fraction bits of binary32, so rounding to nearest-even is adding
+ * half an ulp of the kept part (0x7FFF, plus the kept lsb to break ties towards even) to the 32-bit
+ * pattern and keeping the upper half; a carry out of the fraction correctly bumps the exponent (up to
+ * Inf).  NaN becomes 0x7FC0, the canonical quiet NaN (torch's convention).  Decoding appends 16 zero
+ * bits, which is exact. */
+uint16_t oracle_tr16_encode(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if (x != x) return 0x7FC0u;
+    const uint32_t lsb = (u >> 16) & 1u;
+    return (uint16_t)((u + 0x7FFFu + lsb) >> 16);
+}
+
+float oracle_tr16_decode(uint16_t h) {
+    const uint32_t u = (uint32_t)h << 16;
+    float x;
+    memcpy(&x, &u, 4);
+    return x;
+}
 void oracle_zfp_decode_planes(int64_t ax, int64_t ay, int64_t planes, const uint8_t *src, int rate, float *dst);
 
 /* Bytes of one compressed plane-slab-row: an allocated xy plane of ax*ay
  * values costs ax*ay*rate_bits/8 bytes; identity (codec 0) costs 4 B/value. */
 int64_t oracle_plane_bytes(int64_t ax, int64_t ay, int codec, int q) {
     if (codec == 0) return ax * ay * 4;
+    if (codec == 3) return ax * ay * 2; /* Truncate-16: q unused (rate 16) */
     if (codec == 2) return (ax / 4) * (ay / 4) * 8 * q / 4; /* ZFP: q is the rate (bits/value) */
     return (ax / 4) * (ay / 4) * 8 * (q + 1) / 4;
 }
@@ -229,6 +254,14 @@ int oracle_encode_planes(int64_t ax, int64_t ay, int64_t planes, const float *sr
                          int codec, int q, uint8_t *dst) {
     if (codec == 0) {
         memcpy(dst, src, (size_t)(ax * ay * planes) * 4);
+        return ORACLE_OK;
+    }
+    if (codec == 3) { /* raw bf16 planes, x fastest, little-endian */
+        for (int64_t i = 0; i < ax * ay * planes; ++i) {
+            const uint16_t h = oracle_tr16_encode(src[i]);
+            dst[2 * i] = (uint8_t)(h & 0xFFu);
+            dst[2 * i + 1] = (uint8_t)(h >> 8);
+        }
         return ORACLE_OK;
     }
     if (codec == 2) return oracle_zfp_encode_planes(ax, ay, planes, src, q, dst);
@@ -257,6 +290,11 @@ void oracle_decode_planes(int64_t ax, int64_t ay, int64_t planes, const uint8_t 
                           int codec, int q, float *dst) {
     if (codec == 0) {
         memcpy(dst, src, (size_t)(ax * ay * planes) * 4);
+        return;
+    }
+    if (codec == 3) {
+        for (int64_t i = 0; i < ax * ay * planes; ++i)
+            dst[i] = oracle_tr16_decode((uint16_t)(src[2 * i] | (src[2 * i + 1] << 8)));
         return;
     }
     if (codec == 2) {

@@ -34,13 +34,17 @@ XOFF = 32 - R
 OOCS_OK = 0
 STATUS = {0: "OK", 2: "CONFIG", 3: "DEVICE_OOM", 4: "VERIFY", 5: "IO", 6: "DATA", 7: "HOST_OOM",
           8: "CUDA", 9: "EXCHANGE", 10: "STATE"}
-CODEC = {"identity": 0, "blockquant": 1, "zfp": 2}
+CODEC = {"identity": 0, "blockquant": 1, "zfp": 2, "trunc16": 3}
 MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
 STORE = {"host": 0, "device": 1}
 SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}
 FLAG_PROFILE = 1
 FLAG_RESIDENT_VELOCITY = 2
 FLAG_FUSE_ENCODE = 4
+FLAG_TIMELINE = 8
+FLAG_LANE_SINGLE_STREAM = 16
+FLAG_LANE_SPLIT_STREAMS = 32
+EXECUTOR = {"dispatch": 0, "single": FLAG_LANE_SINGLE_STREAM, "split": FLAG_LANE_SPLIT_STREAMS}
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
 EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY", "NODE"]
 
@@ -87,6 +91,11 @@ class Op(ctypes.Structure):
                 ("pad", i32), ("ev_g", i64)]
 
 
+class Span(ctypes.Structure):
+    _fields_ = [("kind", i32), ("lane", i32), ("g", i64), ("block", i32), ("sweep", i32), ("arg", i32),
+                ("pad", i32), ("start_ms", f64), ("end_ms", f64), ("host_ms", f64)]
+
+
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, vp, i64, vp, vp, vp, vp, u64, vp)
 
 
@@ -121,6 +130,7 @@ def lib():
             "oocs_store_read_raw": ([vp, i32, vp, i64, i64], i32),
             "oocs_store_write_raw": ([vp, i32, vp, i64, i64], i32),
             "oocs_run": ([vp, i64, P(Stats)], i32),
+            "oocs_timeline": ([vp, vp, i64, P(i64)], i32),
             "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
             "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
             "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, vp], i32),
@@ -142,7 +152,8 @@ def _check(st: int, where: str):
 
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
-                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False) -> Config:
+                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False,
+                timeline=False, executor="dispatch") -> Config:
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -157,6 +168,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.store = STORE[store] if isinstance(store, str) else store
     c.device, c.rank, c.world = device, rank, world
     c.flags = ((FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
+               | (FLAG_TIMELINE if timeline else 0) | EXECUTOR[executor]
                | (FLAG_FUSE_ENCODE if fusion else 0))
     c.device_capacity = device_capacity
     return c
@@ -241,6 +253,16 @@ def oocs_run(h, steps: int) -> Stats:
     return st
 
 
+def oocs_timeline(h):
+    """Spans of the last run (OOCS_FLAG_TIMELINE) as dicts, in schedule order."""
+    n = i64(0)
+    _check(lib().oocs_timeline(h, None, 0, ctypes.byref(n)), "oocs_timeline")
+    arr = (Span * n.value)()
+    _check(lib().oocs_timeline(h, arr, n.value, ctypes.byref(n)), "oocs_timeline")
+    return [dict(kind=OP_KINDS[s.kind], lane=s.lane, g=s.g, block=s.block, sweep=s.sweep, arg=s.arg,
+                 start_ms=s.start_ms, end_ms=s.end_ms, host_ms=s.host_ms) for s in arr]
+
+
 def oocs_set_exchange(h, fn, user=None):
     _check(lib().oocs_set_exchange(h, fn, user), "oocs_set_exchange")
 
@@ -290,6 +312,9 @@ class Plan:
 
     def run(self, steps) -> Stats:
         return oocs_run(self.handle, steps)
+
+    def timeline(self):
+        return oocs_timeline(self.handle)
 
     def set_exchange(self, pyfn):
         """pyfn(sweep, send_lo, send_hi, recv_lo, recv_hi, nbytes, stream) -> int (device pointers as ints)."""

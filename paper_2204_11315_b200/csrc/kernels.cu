@@ -7,6 +7,7 @@
 // floats, element x of a row at column x + XOFF (XOFF = 28) so interior x = R
 // starts on a 128-byte line; pitch is a multiple of 32 floats.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -270,6 +271,82 @@ __global__ void id_encode_kernel(const float *__restrict__ src, float4 *__restri
         const int c = (int)(i - row * ax4);
         dst[i] = *reinterpret_cast<const float4 *>(src + row * pitch + XOFF + 4 * c);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Truncate-16 codec: fp32 -> bfloat16 with round-to-nearest-even (the hardware
+// cvt.rn.bf16.f32), NaN -> 0x7FC0; raw bf16 planes, row length ax.  A thread moves 4 words of 8
+// values per iteration, all loads issued before any store (enough bytes in flight per SM to cover
+// HBM latency); blockIdx.y = plane, 32-bit in-plane indices.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t tr16_bits(float x) {
+    return x != x ? 0x7FC0u : (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+// the bf16 side is a flat array: one 16-byte word = 8 values = two 4-groups (ax % 4 == 0, so a
+// 4-group never straddles a row; the two may sit in different rows)
+__device__ __forceinline__ int64_t tr16_ws_off(int q, int ax4, int64_t pitch) {
+    const int row = q / ax4;
+    return row * pitch + 4 * (q - row * ax4);
+}
+
+__global__ void tr16_encode_kernel(const float *__restrict__ src, uint4 *__restrict__ dst, int plane8, int ax4,
+                                   int64_t pitch, int64_t pstride) {
+    const float *s = src + (int64_t)blockIdx.y * pstride + XOFF;
+    uint4 *d = dst + (int64_t)blockIdx.y * plane8;
+    const int stride = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < plane8; i0 += 4 * stride) {
+        float4 v[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * stride;
+            if (i < plane8) {
+                v[j][0] = __ldcs(reinterpret_cast<const float4 *>(s + tr16_ws_off(2 * i, ax4, pitch)));
+                v[j][1] = __ldcs(reinterpret_cast<const float4 *>(s + tr16_ws_off(2 * i + 1, ax4, pitch)));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * stride;
+            if (i < plane8)
+                __stcs(d + i, make_uint4(tr16_bits(v[j][0].x) | tr16_bits(v[j][0].y) << 16,
+                                         tr16_bits(v[j][0].z) | tr16_bits(v[j][0].w) << 16,
+                                         tr16_bits(v[j][1].x) | tr16_bits(v[j][1].y) << 16,
+                                         tr16_bits(v[j][1].z) | tr16_bits(v[j][1].w) << 16));
+        }
+    }
+}
+
+__device__ __forceinline__ float4 tr16_expand(uint32_t lo, uint32_t hi) {
+    return make_float4(__uint_as_float(lo << 16), __uint_as_float(lo & 0xFFFF0000u), __uint_as_float(hi << 16),
+                       __uint_as_float(hi & 0xFFFF0000u));
+}
+
+__global__ void tr16_decode_kernel(const uint4 *__restrict__ src, float *__restrict__ dst, int plane8, int ax4,
+                                   int64_t pitch, int64_t pstride) {
+    const uint4 *s = src + (int64_t)blockIdx.y * plane8;
+    float *d = dst + (int64_t)blockIdx.y * pstride + XOFF;
+    const int stride = gridDim.x * blockDim.x;
+    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < plane8; i0 += 4 * stride) {
+        uint4 u[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i0 + j * stride < plane8) u[j] = __ldcs(s + i0 + j * stride);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * stride;
+            if (i < plane8) {
+                __stcs(reinterpret_cast<float4 *>(d + tr16_ws_off(2 * i, ax4, pitch)), tr16_expand(u[j].x, u[j].y));
+                __stcs(reinterpret_cast<float4 *>(d + tr16_ws_off(2 * i + 1, ax4, pitch)), tr16_expand(u[j].z, u[j].w));
+            }
+        }
+    }
+}
+
+static dim3 tr16_grid(int64_t plane8, int64_t planes) {
+    // about 8 resident 256-thread CTAs per SM over all planes, each thread doing >= 4 words per pass
+    const int64_t want = std::max<int64_t>(1, 148 * 8 / std::max<int64_t>(planes, 1));
+    return dim3((unsigned)std::min<int64_t>((plane8 + 1023) / 1024, want), (unsigned)planes);
 }
 
 // ---------------------------------------------------------------------------
@@ -922,6 +999,16 @@ cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, i
         zfp_decode_kernel<<<grid, 128, 0, st>>>(static_cast<const uint64_t *>(src), dst, nbx, nby, pitch, pstride, q);
         return cudaGetLastError();
     }
+    if (codec == 3) {
+        const int64_t plane8 = ay * ax / 8;  // ax, ay multiples of 4
+        for (int64_t z = 0; z < planes; z += 65535) {  // gridDim.y <= 65535
+            const int64_t n = std::min<int64_t>(planes - z, 65535);
+            tr16_decode_kernel<<<tr16_grid(plane8, n), 256, 0, st>>>(static_cast<const uint4 *>(src) + z * plane8,
+                                                                    dst + z * pstride, (int)plane8, (int)(ax / 4),
+                                                                    pitch, pstride);
+        }
+        return cudaGetLastError();
+    }
     if (codec == 0) {
         const int64_t n4 = planes * ay * (ax / 4);
         const int threads = 256;
@@ -956,6 +1043,16 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
         const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
         const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
         zfp_encode_kernel<<<grid, 128, 0, st>>>(src, static_cast<uint64_t *>(dst), nbx, nby, pitch, pstride, q, err);
+        return cudaGetLastError();
+    }
+    if (codec == 3) {
+        const int64_t plane8 = ay * ax / 8;
+        for (int64_t z = 0; z < planes; z += 65535) {
+            const int64_t n = std::min<int64_t>(planes - z, 65535);
+            tr16_encode_kernel<<<tr16_grid(plane8, n), 256, 0, st>>>(src + z * pstride,
+                                                                    static_cast<uint4 *>(dst) + z * plane8,
+                                                                    (int)plane8, (int)(ax / 4), pitch, pstride);
+        }
         return cudaGetLastError();
     }
     if (codec == 0) {

@@ -24,8 +24,10 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->nx <= 0 || c->ny <= 0 || c->nz <= 0) return bad(err, "grid dimensions must be positive");
     if (c->nx % 4 || c->ny % 4 || c->nz % 4) return bad(err, "nx, ny, nz must be multiples of 4 (4x4x4 codec blocks)");
     if (!(c->dt > 0.0f) || !std::isfinite(c->dt)) return bad(err, "dt must be positive and finite");
-    if (c->codec != OOCS_CODEC_IDENTITY && c->codec != OOCS_CODEC_BLOCKQUANT && c->codec != OOCS_CODEC_ZFP)
+    if (c->codec != OOCS_CODEC_IDENTITY && c->codec != OOCS_CODEC_BLOCKQUANT && c->codec != OOCS_CODEC_ZFP &&
+        c->codec != OOCS_CODEC_TRUNC16)
         return bad(err, "unknown codec");
+    if (c->codec == OOCS_CODEC_TRUNC16 && c->rate_bits != 16) return bad(err, "Truncate-16 has rate_bits 16");
     if (c->codec == OOCS_CODEC_ZFP && (c->rate_bits < 1 || c->rate_bits > 32))
         return bad(err, "ZFP rate_bits must be in [1, 32] (64*rate bits per 4x4x4 block)");
     if (c->codec == OOCS_CODEC_BLOCKQUANT && (c->rate_bits < 2 || c->rate_bits > 24))
@@ -64,8 +66,9 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
     g->codec = c.codec;
     // kernel parameter: q = r - 1 code bits for BlockQuant, the rate itself for ZFP
     g->q = c.codec == OOCS_CODEC_BLOCKQUANT ? c.rate_bits - 1 : c.codec == OOCS_CODEC_ZFP ? c.rate_bits : 0;
-    g->plane_bytes = c.codec == OOCS_CODEC_IDENTITY ? g->ax * g->ay * 4
-                                                    : (g->ax / 4) * (g->ay / 4) * 8 * c.rate_bits / 4;
+    g->plane_bytes = c.codec == OOCS_CODEC_IDENTITY  ? g->ax * g->ay * 4
+                     : c.codec == OOCS_CODEC_TRUNC16 ? g->ax * g->ay * 2
+                                                     : (g->ax / 4) * (g->ay / 4) * 8 * c.rate_bits / 4;
     g->k = c.tb_depth;
     const int n = c.n_blocks;
     const int64_t kR = (int64_t)c.tb_depth * R;

@@ -5,10 +5,13 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "oocs_internal.h"
@@ -51,7 +54,14 @@ struct Plan {
     uint8_t *xbuf[4] = {};           // exchange buffers: send_lo, send_hi, recv_lo, recv_hi
     uint64_t xbytes = 0;
     int *d_err = nullptr;
-    cudaStream_t lanes[MAX_LANES] = {};
+    cudaStream_t lanes[MAX_LANES] = {};   // copy stream of each lane (and its kernels with LANE_SINGLE_STREAM)
+    cudaStream_t klanes[MAX_LANES] = {};  // kernel stream of each lane (== lanes[] with LANE_SINGLE_STREAM)
+    cudaEvent_t xfer_ev[MAX_LANES] = {}, kdone[MAX_LANES] = {};
+    bool split = false;
+    cudaStream_t cstream[3] = {};           // dispatcher: H2D, D2H and D2D (carry) copy streams
+    cudaEvent_t cdone[3] = {};
+    std::vector<cudaEvent_t> op_done;       // dispatcher: completion event of every op of a run
+    uint64_t copy_chunk = 0;  // pipeline PCIe copies are issued in pieces of this many bytes (0: whole)
     std::vector<cudaEvent_t> ev[6];  // per oocs_event_kind, rings indexed by block counter / DAG node
     int ev_ring = 0;
     cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[MAX_LANES] = {};
@@ -60,6 +70,10 @@ struct Plan {
     bool poisoned = false;
     std::vector<KernelTiming> timing_pool;
     size_t timing_used = 0;
+    // OOCS_FLAG_TIMELINE: one event pair per work op (pool reused across runs) and the last run's spans
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> span_events;
+    std::vector<oocs_span> spans;
+    std::chrono::steady_clock::time_point host_t0;
 };
 
 }  // namespace oocs
@@ -96,15 +110,43 @@ static oocs_status poison(Plan *p, oocs_status st) {
     return st;
 }
 
-// pitched 2D copy of `planes` allocated planes between raw (row = ax floats)
-// and working-buffer layout
+// Pipeline PCIe copies can go out in pieces of `chunk` bytes (OOCS_COPY_CHUNK_MB, default 0 = whole
+// copies): an experiment against the copy-engine stalls of DESIGN.md §8 -- measured, pieces of 2-32 MB
+// lower the achieved PCIe rate and do not remove the stalls (the host dispatcher does).
+static cudaError_t copy_1d(void *dst, const void *src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t st,
+                           uint64_t chunk) {
+    if (!chunk) chunk = bytes;
+    for (uint64_t o = 0; o < bytes; o += chunk) {
+        cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t *>(dst) + o, static_cast<const uint8_t *>(src) + o,
+                                        std::min(chunk, bytes - o), kind, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// pitched 2D copy of `planes` allocated planes between raw (row = ax floats) and working-buffer
+// layout, in pieces of whole rows of about `chunk` bytes
 static cudaError_t copy_raw_to_ws(float *ws_plane0, const void *raw, const Geometry &g, int64_t planes,
-                                  cudaMemcpyKind kind, cudaStream_t st) {
-    return cudaMemcpy2DAsync(ws_plane0 + XOFF, g.pitch * 4, raw, g.ax * 4, g.ax * 4, planes * g.ay, kind, st);
+                                  cudaMemcpyKind kind, cudaStream_t st, uint64_t chunk = 0) {
+    const int64_t rows = planes * g.ay, step = chunk ? std::max<int64_t>(1, (int64_t)(chunk / (g.ax * 4))) : rows;
+    for (int64_t r = 0; r < rows; r += step) {
+        cudaError_t e = cudaMemcpy2DAsync(ws_plane0 + XOFF + r * g.pitch, g.pitch * 4,
+                                          static_cast<const float *>(raw) + r * g.ax, g.ax * 4, g.ax * 4,
+                                          std::min(step, rows - r), kind, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 static cudaError_t copy_ws_to_raw(void *raw, const float *ws_plane0, const Geometry &g, int64_t planes,
-                                  cudaMemcpyKind kind, cudaStream_t st) {
-    return cudaMemcpy2DAsync(raw, g.ax * 4, ws_plane0 + XOFF, g.pitch * 4, g.ax * 4, planes * g.ay, kind, st);
+                                  cudaMemcpyKind kind, cudaStream_t st, uint64_t chunk = 0) {
+    const int64_t rows = planes * g.ay, step = chunk ? std::max<int64_t>(1, (int64_t)(chunk / (g.ax * 4))) : rows;
+    for (int64_t r = 0; r < rows; r += step) {
+        cudaError_t e = cudaMemcpy2DAsync(static_cast<float *>(raw) + r * g.ax, g.ax * 4,
+                                          ws_plane0 + XOFF + r * g.pitch, g.pitch * 4, g.ax * 4,
+                                          std::min(step, rows - r), kind, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -196,6 +238,16 @@ static void free_plan(Plan *p) {
     int cur_dev = -1;
     cudaGetDevice(&cur_dev);
     cudaSetDevice(p->geo.cfg.device);
+    for (int c = 0; c < 3; ++c) {
+        if (p->cstream[c]) cudaStreamDestroy(p->cstream[c]);
+        if (p->cdone[c]) cudaEventDestroy(p->cdone[c]);
+    }
+    for (auto e : p->op_done) cudaEventDestroy(e);
+    for (int l = 0; l < MAX_LANES; ++l) {
+        if (p->split && p->klanes[l]) cudaStreamDestroy(p->klanes[l]);
+        if (p->xfer_ev[l]) cudaEventDestroy(p->xfer_ev[l]);
+        if (p->kdone[l]) cudaEventDestroy(p->kdone[l]);
+    }
     for (auto &s : p->lanes)
         if (s) cudaStreamDestroy(s);
     for (auto &v : p->ev)
@@ -207,6 +259,10 @@ static void free_plan(Plan *p) {
     for (auto &t : p->timing_pool) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
+    }
+    for (auto &e : p->span_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
     }
     if (p->arena.owned && p->arena.base) cudaFree(p->arena.base);
     for (auto h : p->hstore)
@@ -346,13 +402,31 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
             std::memset(p->hstore[a], 0, arr_store);
         }
     }
-    for (int l = 0; l < g.lanes; ++l) {
-        if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&p->lane_done[l], cudaEventDisableTiming) != cudaSuccess) {
+    // a kernel stream per lane for the dispatcher and the split replay; the lane's own stream otherwise
+    p->split = !(g.cfg.flags & OOCS_FLAG_LANE_SINGLE_STREAM);
+    for (int c = 0; c < 3; ++c)
+        if (cudaStreamCreateWithFlags(&p->cstream[c], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->cdone[c], cudaEventDisableTiming) != cudaSuccess) {
             set_error("stream/event creation failed");
             free_plan(p);
             return OOCS_ERR_CUDA;
         }
+    {
+        // piece size of the pipeline's PCIe copies (OOCS_COPY_CHUNK_MB overrides; 0 = whole copies)
+        const char *env = std::getenv("OOCS_COPY_CHUNK_MB");
+        p->copy_chunk = (env ? (uint64_t)std::strtoull(env, nullptr, 10) : 0ull) << 20;
+    }
+    for (int l = 0; l < g.lanes; ++l) {
+        if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->lane_done[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->xfer_ev[l], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->kdone[l], cudaEventDisableTiming) != cudaSuccess ||
+            (p->split && cudaStreamCreateWithFlags(&p->klanes[l], cudaStreamNonBlocking) != cudaSuccess)) {
+            set_error("stream/event creation failed");
+            free_plan(p);
+            return OOCS_ERR_CUDA;
+        }
+        if (!p->split) p->klanes[l] = p->lanes[l];
     }
     p->ev_ring = g.nb() + 8;
     // DAG node events: a wait always refers to a node at most `window` chunks back (plan.cpp)
@@ -386,7 +460,11 @@ static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
     const int64_t kR = (int64_t)g.k * R;
     const int64_t Zlo = g.blocks[g.b_lo].own_lo, Zhi = g.blocks[g.b_hi - 1].own_hi;
     const bool has_lo = g.cfg.rank > 0, has_hi = g.cfg.rank + 1 < g.cfg.world;
-    for (int l = 0; l < g.lanes; ++l) CU(cudaStreamSynchronize(p->lanes[l]));
+    for (int l = 0; l < g.lanes; ++l) {
+        CU(cudaStreamSynchronize(p->lanes[l]));
+        CU(cudaStreamSynchronize(p->klanes[l]));
+    }
+    for (int c = 0; c < 3; ++c) CU(cudaStreamSynchronize(p->cstream[c]));
     cudaStream_t st = p->lanes[0];
     const uint64_t arr = (uint64_t)kR * pb(p);
     // pack: planes [Zlo, Zlo+kR) -> send_lo ; [Zhi-kR, Zhi) -> send_hi ; arrays 1, 2
@@ -429,149 +507,360 @@ static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
     return OOCS_OK;
 }
 
-static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats *stats) {
+// Issue one work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) on stream st.  The device
+// store's read/write buffers follow from the op's sweep: S_t = dstore[cur0 ^ (sweep & 1)].
+static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cur0, oocs_stats *stats) {
     const Geometry &g = p->geo;
-    const int64_t kR = (int64_t)g.k * R;
     const uint64_t PB = pb(p);
-    const int nb = g.nb();
-    auto blk = [&](const oocs_op &o) -> const oocs_block & { return g.blocks[o.block]; };
-    for (const oocs_op &o : ops) {
-        cudaStream_t st = p->lanes[o.lane];
-        const oocs_block &b = blk(o);
-        const int64_t E = b.ext_hi - b.ext_lo;
-        const int w = (int)(o.g % g.n_ws);
-        const int s = (int)(o.g % g.lanes);
-        switch (o.kind) {
-        case OOCS_OP_WAIT:
-            CU(cudaStreamWaitEvent(st, evt(p, o.arg, o.ev_g), 0));
-            break;
-        case OOCS_OP_RECORD:
-            CU(cudaEventRecord(evt(p, o.arg, o.ev_g), st));
-            break;
-        case OOCS_OP_H2D: {
-            const int64_t nplanes = b.body_hi - b.body_lo, off = b.body_lo - b.ext_lo;
-            if (g.cfg.mode == OOCS_MODE_BASELINE) {
-                for (int a = 0; a < N_ARRAYS; ++a)
-                    CU(copy_raw_to_ws(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), g, nplanes,
-                                      cudaMemcpyHostToDevice, st));
-            } else {
-                for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
-                    CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB,
-                                       p->hstore[a] + hoff(p, b.body_lo), nplanes * PB, cudaMemcpyHostToDevice, st));
-            }
-            if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
-            break;
+    const oocs_block &b = g.blocks[o.block];
+    const int64_t E = b.ext_hi - b.ext_lo;
+    const int w = (int)(o.g % g.n_ws);
+    const int s = (int)(o.g % g.lanes);
+    p->cur = cur0 ^ (o.sweep & 1);
+    switch (o.kind) {
+    case OOCS_OP_WAIT:
+        CU(cudaStreamWaitEvent(st, evt(p, o.arg, o.ev_g), 0));
+        break;
+    case OOCS_OP_RECORD:
+        CU(cudaEventRecord(evt(p, o.arg, o.ev_g), st));
+        break;
+    case OOCS_OP_H2D: {
+        const int64_t nplanes = b.body_hi - b.body_lo, off = b.body_lo - b.ext_lo;
+        if (g.cfg.mode == OOCS_MODE_BASELINE) {
+            for (int a = 0; a < N_ARRAYS; ++a)
+                CU(copy_raw_to_ws(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), g, nplanes,
+                                  cudaMemcpyHostToDevice, st, p->copy_chunk));
+        } else {
+            for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
+                CU(copy_1d(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB, p->hstore[a] + hoff(p, b.body_lo),
+                           nplanes * PB, cudaMemcpyHostToDevice, st, p->copy_chunk));
         }
-        case OOCS_OP_CARRY: {
-            // overlap of this chunk with the previous chunk's extent, already on the GPU
-            const oocs_block &pbk = g.blocks[o.block - 1];
-            const int64_t nplanes = b.carry_hi - b.carry_lo;
-            const int64_t src_off = b.carry_lo - pbk.ext_lo, dst_off = b.carry_lo - b.ext_lo;
-            if (g.cfg.mode == OOCS_MODE_BASELINE) {
-                // lane of o is the previous chunk's lane; destination is chunk g's working set
-                const int wprev = (int)((o.g - 1) % g.n_ws);
-                for (int a = 0; a < N_ARRAYS; ++a)
-                    CU(cudaMemcpy2DAsync(wsa(p, w, a) + dst_off * g.pstride, g.pitch * 4,
-                                         wsa(p, wprev, a) + src_off * g.pstride, g.pitch * 4, g.pitch * 4,
-                                         nplanes * g.ay, cudaMemcpyDeviceToDevice, st));
-                if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
-            } else {
-                const int sp = (int)((o.g - 1) % g.lanes);
-                for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
-                    CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
-                                       p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
-                                       cudaMemcpyDeviceToDevice, st));
-                if (stats) stats->bytes_d2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
-            }
-            break;
+        if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
+        break;
+    }
+    case OOCS_OP_CARRY: {
+        // overlap of this chunk with the previous chunk's extent, already on the GPU
+        const oocs_block &pbk = g.blocks[o.block - 1];
+        const int64_t nplanes = b.carry_hi - b.carry_lo;
+        const int64_t src_off = b.carry_lo - pbk.ext_lo, dst_off = b.carry_lo - b.ext_lo;
+        if (g.cfg.mode == OOCS_MODE_BASELINE) {
+            // lane of o is the previous chunk's lane; destination is chunk g's working set
+            const int wprev = (int)((o.g - 1) % g.n_ws);
+            for (int a = 0; a < N_ARRAYS; ++a)
+                CU(cudaMemcpy2DAsync(wsa(p, w, a) + dst_off * g.pstride, g.pitch * 4,
+                                     wsa(p, wprev, a) + src_off * g.pstride, g.pitch * 4, g.pitch * 4,
+                                     nplanes * g.ay, cudaMemcpyDeviceToDevice, st));
+            if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
+        } else {
+            const int sp = (int)((o.g - 1) % g.lanes);
+            for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
+                CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
+                                   p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
+                                   cudaMemcpyDeviceToDevice, st));
+            if (stats) stats->bytes_d2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
         }
-        case OOCS_OP_DECODE: {
-            for (int a = 0; a < N_ARRAYS; ++a) {
-                const uint8_t *src;
-                if (a == 0 && p->resident_vel)
-                    src = p->dvel + hoff(p, b.ext_lo);
-                else if (g.host_store)
-                    src = p->hf[s] + (uint64_t)a * g.max_ext * PB;
-                else
-                    src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
-                oocs_status r = k_decode(p, src, wsa(p, w, a), E, st, stats);
-                if (r) return r;
-            }
-            break;
+        break;
+    }
+    case OOCS_OP_DECODE: {
+        for (int a = 0; a < N_ARRAYS; ++a) {
+            const uint8_t *src;
+            if (a == 0 && p->resident_vel)
+                src = p->dvel + hoff(p, b.ext_lo);
+            else if (g.host_store)
+                src = p->hf[s] + (uint64_t)a * g.max_ext * PB;
+            else
+                src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
+            oocs_status r = k_decode(p, src, wsa(p, w, a), E, st, stats);
+            if (r) return r;
         }
-        case OOCS_OP_STEP: {
-            // step s is valid on [lo_s, hi_s): the trapezoid shrinks by R per step except at
-            // the physical boundary (P:L85 temporal blocking)
-            const int sidx = o.arg;
-            const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
-            const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
-            const int up = upd_array(sidx), other = 3 - up;
-            if (fuse_last_step(p) && sidx == g.k) {
-                // the last step and the encode of the owned slabs in one kernel: level k is never
-                // written back, (level k-1, level k) go straight to S_{t+1}'s records
-                void *out_prev = p->dstore[p->cur ^ 1][1] + hoff(p, b.own_lo);
-                void *out_curr = p->dstore[p->cur ^ 1][2] + hoff(p, b.own_lo);
-                oocs_status r = k_step_encode(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
-                                              hi - b.ext_lo, out_prev, out_curr, st, stats);
-                if (r) return r;
-                break;
-            }
-            oocs_status r = k_step(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo, st,
-                                   stats);
+        break;
+    }
+    case OOCS_OP_STEP: {
+        // step s is valid on [lo_s, hi_s): the trapezoid shrinks by R per step except at
+        // the physical boundary (P:L85 temporal blocking)
+        const int sidx = o.arg;
+        const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
+        const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
+        const int up = upd_array(sidx), other = 3 - up;
+        if (fuse_last_step(p) && sidx == g.k) {
+            // the last step and the encode of the owned slabs in one kernel: level k is never
+            // written back, (level k-1, level k) go straight to S_{t+1}'s records
+            void *out_prev = p->dstore[p->cur ^ 1][1] + hoff(p, b.own_lo);
+            void *out_curr = p->dstore[p->cur ^ 1][2] + hoff(p, b.own_lo);
+            oocs_status r = k_step_encode(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
+                                          hi - b.ext_lo, out_prev, out_curr, st, stats);
             if (r) return r;
             break;
         }
-        case OOCS_OP_ENCODE: {
-            if (fuse_last_step(p)) break;  // done by the fused last step
-            // after k steps: level t0+k in array upd(k), level t0+k-1 in the other
+        oocs_status r = k_step(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo, st,
+                               stats);
+        if (r) return r;
+        break;
+    }
+    case OOCS_OP_ENCODE: {
+        if (fuse_last_step(p)) break;  // done by the fused last step
+        // after k steps: level t0+k in array upd(k), level t0+k-1 in the other
+        const int curr = upd_array(g.k), prev = 3 - curr;
+        const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;
+        const int src_arr[2] = {prev, curr};
+        for (int j = 0; j < 2; ++j) {
+            void *dst;
+            if (g.host_store)
+                dst = p->hf[s] + (uint64_t)j * g.max_own * PB;
+            else
+                dst = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
+            oocs_status r = k_encode(p, wsa(p, w, src_arr[j]) + off * g.pstride, dst, W, st, stats);
+            if (r) return r;
+        }
+        break;
+    }
+    case OOCS_OP_D2H: {
+        const int64_t W = b.own_hi - b.own_lo;
+        if (g.cfg.mode == OOCS_MODE_BASELINE) {
             const int curr = upd_array(g.k), prev = 3 - curr;
-            const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;
-            const int src_arr[2] = {prev, curr};
-            for (int j = 0; j < 2; ++j) {
-                void *dst;
-                if (g.host_store)
-                    dst = p->hf[s] + (uint64_t)j * g.max_own * PB;
-                else
-                    dst = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
-                oocs_status r = k_encode(p, wsa(p, w, src_arr[j]) + off * g.pstride, dst, W, st, stats);
-                if (r) return r;
-            }
-            break;
+            const int64_t off = b.own_lo - b.ext_lo;
+            CU(copy_ws_to_raw(p->hstore[1] + hoff(p, b.own_lo), wsa(p, w, prev) + off * g.pstride, g, W,
+                              cudaMemcpyDeviceToHost, st, p->copy_chunk));
+            CU(copy_ws_to_raw(p->hstore[2] + hoff(p, b.own_lo), wsa(p, w, curr) + off * g.pstride, g, W,
+                              cudaMemcpyDeviceToHost, st, p->copy_chunk));
+        } else {
+            for (int j = 0; j < 2; ++j)
+                CU(copy_1d(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf[s] + (uint64_t)j * g.max_own * PB, W * PB,
+                           cudaMemcpyDeviceToHost, st, p->copy_chunk));
         }
-        case OOCS_OP_D2H: {
-            const int64_t W = b.own_hi - b.own_lo;
-            if (g.cfg.mode == OOCS_MODE_BASELINE) {
-                const int curr = upd_array(g.k), prev = 3 - curr;
-                const int64_t off = b.own_lo - b.ext_lo;
-                CU(copy_ws_to_raw(p->hstore[1] + hoff(p, b.own_lo), wsa(p, w, prev) + off * g.pstride, g, W,
-                                  cudaMemcpyDeviceToHost, st));
-                CU(copy_ws_to_raw(p->hstore[2] + hoff(p, b.own_lo), wsa(p, w, curr) + off * g.pstride, g, W,
-                                  cudaMemcpyDeviceToHost, st));
-            } else {
-                for (int j = 0; j < 2; ++j)
-                    CU(cudaMemcpyAsync(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf[s] + (uint64_t)j * g.max_own * PB,
-                                       W * PB, cudaMemcpyDeviceToHost, st));
-            }
-            if (stats) stats->bytes_d2h += (uint64_t)2 * W * PB;
-            break;
+        if (stats) stats->bytes_d2h += (uint64_t)2 * W * PB;
+        break;
+    }
+    case OOCS_OP_EXCHANGE: {
+        oocs_status r = do_exchange(p, o.sweep, stats);
+        if (r) return r;
+        if (!g.host_store) p->cur ^= 1;
+        break;
+    }
+    default:
+        set_error("internal: unknown op");
+        return OOCS_ERR_STATE;
+    }
+    return OOCS_OK;
+}
+
+static bool is_kernel_op(int k) { return k == OOCS_OP_DECODE || k == OOCS_OP_STEP || k == OOCS_OP_ENCODE; }
+static bool is_work_op(int k) { return k != OOCS_OP_WAIT && k != OOCS_OP_RECORD; }
+
+// OOCS_FLAG_TIMELINE: event pair around a work op
+static oocs_status span_begin(Plan *p, const oocs_op &o, cudaStream_t st, size_t *idx) {
+    const size_t n = p->spans.size();
+    if (n == p->span_events.size()) {
+        cudaEvent_t a, e;
+        CU(cudaEventCreate(&a));
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            cudaEventDestroy(a);
+            CU(cudaErrorMemoryAllocation);
         }
-        case OOCS_OP_EXCHANGE: {
-            oocs_status r = do_exchange(p, o.sweep, stats);
-            if (r) return r;
-            if (!g.host_store) p->cur ^= 1;
-            break;
+        p->span_events.emplace_back(a, e);
+    }
+    oocs_span sp{};
+    sp.kind = o.kind;
+    sp.lane = o.lane;
+    sp.g = o.g;
+    sp.block = o.block;
+    sp.sweep = o.sweep;
+    sp.arg = o.arg;
+    sp.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - p->host_t0).count();
+    p->spans.push_back(sp);
+    CU(cudaEventRecord(p->span_events[n].first, st));
+    *idx = n;
+    return OOCS_OK;
+}
+
+// Executor 1 (OOCS_FLAG_LANE_SINGLE_STREAM / OOCS_FLAG_LANE_SPLIT_STREAMS): the schedule replayed onto
+// CUDA streams in list order -- every lane one stream (Alg. 1 literally), or a copy and a kernel
+// stream per lane joined by an event at every switch.  WAIT/RECORD become cudaStreamWaitEvent /
+// cudaEventRecord.
+static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int cur0, oocs_stats *stats) {
+    const Geometry &g = p->geo;
+    const bool tl = g.cfg.flags & OOCS_FLAG_TIMELINE;
+    // a WAIT goes to the stream of the lane's next work op, a RECORD to the stream of its previous one
+    auto work_stream = [&](const oocs_op &o) {
+        return o.kind == OOCS_OP_EXCHANGE ? p->lanes[0] : is_kernel_op(o.kind) ? p->klanes[o.lane] : p->lanes[o.lane];
+    };
+    std::vector<cudaStream_t> op_stream(ops.size());
+    {
+        std::vector<cudaStream_t> next(g.lanes, nullptr), prev(g.lanes, nullptr);
+        for (size_t i = ops.size(); i-- > 0;) {
+            const oocs_op &o = ops[i];
+            if (is_work_op(o.kind)) next[o.lane] = work_stream(o);
+            else if (o.kind == OOCS_OP_WAIT) op_stream[i] = next[o.lane] ? next[o.lane] : p->lanes[o.lane];
         }
-        default:
-            set_error("internal: unknown op");
-            return OOCS_ERR_STATE;
-        }
-        // device store: the sweep ends after the last chunk's ENCODE (single lane, in order)
-        if (!g.host_store && o.kind == OOCS_OP_ENCODE && o.g % nb == nb - 1) {
-            const bool exch_follows = g.cfg.world > 1 && (&o != &ops.back()) && (&o + 1)->kind == OOCS_OP_EXCHANGE;
-            if (!exch_follows) p->cur ^= 1;
+        for (size_t i = 0; i < ops.size(); ++i) {
+            const oocs_op &o = ops[i];
+            if (is_work_op(o.kind)) op_stream[i] = prev[o.lane] = work_stream(o);
+            else if (o.kind == OOCS_OP_RECORD) op_stream[i] = prev[o.lane] ? prev[o.lane] : p->lanes[o.lane];
         }
     }
-    (void)kR;
+    std::vector<cudaStream_t> last_work(g.lanes, nullptr);
+    for (size_t oi = 0; oi < ops.size(); ++oi) {
+        const oocs_op &o = ops[oi];
+        cudaStream_t st = op_stream[oi];
+        if (o.kind == OOCS_OP_WAIT) {
+            CU(cudaStreamWaitEvent(st, evt(p, o.arg, o.ev_g), 0));
+            continue;
+        }
+        if (o.kind == OOCS_OP_RECORD) {
+            CU(cudaEventRecord(evt(p, o.arg, o.ev_g), st));
+            continue;
+        }
+        if (o.kind != OOCS_OP_EXCHANGE) {
+            // program order within the lane across its two streams
+            cudaStream_t &lw = last_work[o.lane];
+            if (lw && lw != st) {
+                CU(cudaEventRecord(p->xfer_ev[o.lane], lw));
+                CU(cudaStreamWaitEvent(st, p->xfer_ev[o.lane], 0));
+            }
+            lw = st;
+        }
+        size_t sp = 0;
+        if (tl) {
+            oocs_status r = span_begin(p, o, st, &sp);
+            if (r) return r;
+        }
+        oocs_status r = issue_work(p, o, st, cur0, stats);
+        if (r) return r;
+        if (tl) CU(cudaEventRecord(p->span_events[sp].second, o.kind == OOCS_OP_EXCHANGE ? p->lanes[0] : st));
+    }
+    return OOCS_OK;
+}
+
+// Executor 2 (default): a host dispatcher over the schedule's dependency graph.  Every WAIT of the
+// lowered schedule is resolved to the work op whose completion its event marks, and every work op
+// depends on the previous work op of its lane (the lane's program order).  Kernels are issued in list
+// order on their lane's kernel stream as soon as their dependencies are issued, with device-side
+// waits on the dependencies' completion events.  A copy (H2D, CARRY, D2H) is issued only once its
+// dependencies have COMPLETED (polled with cudaEventQuery), onto one stream per direction, so no copy
+// stream ever holds a pending cross-stream wait: a copy channel blocked on a wait is re-examined by
+// the copy-engine scheduler only between DMA commands, and with stream-mapped waits the decode of chunk
+// g was measured to start only once the H2D of chunk g+1 had finished.  Same
+// dependencies as the stream-mapped replay, so the same bytes.
+static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, int cur0, oocs_stats *stats) {
+    const Geometry &g = p->geo;
+    const bool tl = g.cfg.flags & OOCS_FLAG_TIMELINE;
+    const size_t n = ops.size();
+    // producer of every event instance (kind, block counter) and the dependency lists
+    std::vector<int64_t> dep_start(n + 1, 0), deps;
+    {
+        std::vector<int64_t> last_work(g.lanes, -1), pending;
+        std::vector<std::vector<int64_t>> producer(6);
+        auto key = [&](int kind, int64_t eg) -> int64_t & {
+            auto &v = producer[kind];
+            const int64_t i = eg + 1;  // ev_g >= -1
+            if ((int64_t)v.size() <= i) v.resize(i + 1, -1);
+            return v[i];
+        };
+        std::vector<std::vector<int64_t>> lane_waits(g.lanes);
+        for (size_t i = 0; i < n; ++i) {
+            const oocs_op &o = ops[i];
+            dep_start[i] = (int64_t)deps.size();
+            if (o.kind == OOCS_OP_RECORD) {
+                key(o.arg, o.ev_g) = last_work[o.lane];  // -1: records nothing (trivially complete)
+            } else if (o.kind == OOCS_OP_WAIT) {
+                const int64_t pr = key(o.arg, o.ev_g);
+                if (pr >= 0) lane_waits[o.lane].push_back(pr);
+            } else {
+                if (o.kind == OOCS_OP_EXCHANGE) {
+                    for (size_t j = 0; j < i; ++j)  // a host-synchronous barrier over everything before it
+                        if (is_work_op(ops[j].kind)) deps.push_back((int64_t)j);
+                } else {
+                    if (last_work[o.lane] >= 0) deps.push_back(last_work[o.lane]);
+                    for (int64_t d : lane_waits[o.lane]) deps.push_back(d);
+                }
+                lane_waits[o.lane].clear();
+                last_work[o.lane] = (int64_t)i;
+            }
+        }
+        dep_start[n] = (int64_t)deps.size();
+    }
+    if (p->op_done.size() < n) {
+        const size_t old = p->op_done.size();
+        p->op_done.resize(n, nullptr);
+        for (size_t i = old; i < n; ++i)
+            if (cudaEventCreateWithFlags(&p->op_done[i], cudaEventDisableTiming) != cudaSuccess) {
+                p->op_done.resize(i);
+                CU(cudaErrorMemoryAllocation);
+            }
+    }
+    auto stream_of = [&](const oocs_op &o) -> cudaStream_t {
+        switch (o.kind) {
+        case OOCS_OP_H2D: return p->cstream[0];
+        case OOCS_OP_D2H: return p->cstream[1];
+        case OOCS_OP_CARRY: return p->cstream[2];
+        case OOCS_OP_EXCHANGE: return p->lanes[0];
+        default: return p->klanes[o.lane];
+        }
+    };
+    std::vector<char> issued(n, 0), done(n, 0);
+    std::vector<cudaStream_t> where(n, nullptr);
+    for (size_t i = 0; i < n; ++i)
+        if (!is_work_op(ops[i].kind)) issued[i] = done[i] = 1;
+    auto complete = [&](int64_t d) -> bool {
+        if (done[d]) return true;
+        const cudaError_t e = cudaEventQuery(p->op_done[d]);
+        if (e == cudaSuccess) return done[d] = 1;
+        if (e != cudaErrorNotReady) (void)cudaGetLastError();
+        return false;
+    };
+    size_t first = 0;
+    while (first < n) {
+        bool progress = false;
+        for (size_t i = first; i < n; ++i) {
+            if (issued[i]) continue;
+            const oocs_op &o = ops[i];
+            const bool copy = !is_kernel_op(o.kind) && o.kind != OOCS_OP_EXCHANGE;
+            bool ready = true;
+            for (int64_t k = dep_start[i]; k < dep_start[i + 1] && ready; ++k) {
+                const int64_t d = deps[k];
+                ready = issued[d] && (!(copy || o.kind == OOCS_OP_EXCHANGE) || complete(d));
+            }
+            if (!ready) {
+                if (o.kind == OOCS_OP_EXCHANGE) break;  // a barrier: nothing after it may pass
+                continue;
+            }
+            cudaStream_t st = stream_of(o);
+            if (!copy && o.kind != OOCS_OP_EXCHANGE)
+                for (int64_t k = dep_start[i]; k < dep_start[i + 1]; ++k) {
+                    const int64_t d = deps[k];
+                    if (where[d] != st && !done[d]) CU(cudaStreamWaitEvent(st, p->op_done[d], 0));
+                }
+            if (o.kind == OOCS_OP_EXCHANGE)
+                for (int c = 0; c < 3; ++c) CU(cudaStreamSynchronize(p->cstream[c]));
+            size_t sp = 0;
+            if (tl) {
+                oocs_status r = span_begin(p, o, st, &sp);
+                if (r) return r;
+            }
+            oocs_status r = issue_work(p, o, st, cur0, stats);
+            if (r) return r;
+            if (tl) CU(cudaEventRecord(p->span_events[sp].second, st));
+            CU(cudaEventRecord(p->op_done[i], st));
+            issued[i] = 1;
+            where[i] = st;
+            progress = true;
+        }
+        while (first < n && issued[first]) ++first;
+        if (!progress) std::this_thread::yield();
+    }
+    return OOCS_OK;
+}
+
+static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats *stats) {
+    const Geometry &g = p->geo;
+    const int cur0 = p->cur;
+    int64_t sweeps = 0;
+    for (const oocs_op &o : ops) sweeps = std::max<int64_t>(sweeps, o.sweep + 1);
+    oocs_status r = (g.cfg.flags & (OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS))
+                        ? execute_streams(p, ops, cur0, stats)
+                        : execute_dispatch(p, ops, cur0, stats);
+    if (r) return r;
+    p->cur = g.host_store ? cur0 : cur0 ^ (int)(sweeps & 1);
     return OOCS_OK;
 }
 
@@ -591,14 +880,28 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
     std::vector<oocs_op> ops;
     lower_schedule(g, steps / g.k, ops);
     p->timing_used = 0;
+    p->spans.clear();
+    p->host_t0 = std::chrono::steady_clock::now();
     CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->lanes[0]));
     CU(cudaEventRecord(p->t0, p->lanes[0]));
     for (int l = 1; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0, 0));
+    if (p->split)
+        for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->klanes[l], p->t0, 0));
+    for (int c = 0; c < 3; ++c) CU(cudaStreamWaitEvent(p->cstream[c], p->t0, 0));
     oocs_status st = execute(p, ops, &stats);
     if (st) return poison(p, st);
     for (int l = 1; l < g.lanes; ++l) {
         CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
         CU(cudaStreamWaitEvent(p->lanes[0], p->lane_done[l], 0));
+    }
+    if (p->split)
+        for (int l = 0; l < g.lanes; ++l) {
+            CU(cudaEventRecord(p->kdone[l], p->klanes[l]));
+            CU(cudaStreamWaitEvent(p->lanes[0], p->kdone[l], 0));
+        }
+    for (int c = 0; c < 3; ++c) {
+        CU(cudaEventRecord(p->cdone[c], p->cstream[c]));
+        CU(cudaStreamWaitEvent(p->lanes[0], p->cdone[c], 0));
     }
     CU(cudaEventRecord(p->t1, p->lanes[0]));
     CU(cudaEventSynchronize(p->t1));
@@ -609,6 +912,13 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
         float t = 0.f;
         CU(cudaEventElapsedTime(&t, p->timing_pool[i].a, p->timing_pool[i].b));
         stats.kernel_ms[p->timing_pool[i].kind] += t;
+    }
+    for (size_t i = 0; i < p->spans.size(); ++i) {
+        float a = 0.f, b = 0.f;
+        CU(cudaEventElapsedTime(&a, p->t0, p->span_events[i].first));
+        CU(cudaEventElapsedTime(&b, p->t0, p->span_events[i].second));
+        p->spans[i].start_ms = a;
+        p->spans[i].end_ms = b;
     }
     int herr = 0;
     CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -819,10 +1129,24 @@ oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out) {
     return poison(plan, run(plan, steps, out));
 }
 
+oocs_status oocs_timeline(const oocs_plan *plan, oocs_span *out, int64_t cap, int64_t *n_spans) {
+    if (oocs_status st = guard(plan)) return st;
+    if (!n_spans || cap < 0) {
+        set_error("oocs_timeline: n_spans is NULL or cap < 0");
+        return OOCS_ERR_CONFIG;
+    }
+    const int64_t n = (int64_t)plan->spans.size();
+    *n_spans = n;
+    if (out)
+        for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = plan->spans[i];
+    return OOCS_OK;
+}
+
 oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
                         int32_t codec, int32_t rate_bits, void *stream) {
-    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 2 ||
-        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32))) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 3 ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32)) ||
+        (codec == 3 && rate_bits != 16)) {
         set_error("oocs_decode: bad geometry or codec");
         return OOCS_ERR_CONFIG;
     }
@@ -833,8 +1157,9 @@ oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int
 
 oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
                         int32_t codec, int32_t rate_bits, int32_t *err_flag, void *stream) {
-    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 2 ||
-        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32))) {
+    if (ax % 4 || ay % 4 || planes % 4 || pitch < ax + XOFF || pitch % 32 || codec < 0 || codec > 3 ||
+        (codec == 1 && (rate_bits < 2 || rate_bits > 24)) || (codec == 2 && (rate_bits < 1 || rate_bits > 32)) ||
+        (codec == 3 && rate_bits != 16)) {
         set_error("oocs_encode: bad geometry or codec");
         return OOCS_ERR_CONFIG;
     }

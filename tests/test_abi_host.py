@@ -40,7 +40,8 @@ def cfg(**kw):
 @pytest.mark.parametrize("kw", [
     dict(nx=63), dict(nz=0), dict(n_blocks=17), dict(tb_depth=4), dict(rate_bits=25), dict(rate_bits=1),
     dict(mode="baseline", codec="blockquant"), dict(world=3), dict(rank=4, world=4), dict(dt=-1.0),
-    dict(region_sharing=False, store="host"), dict(codec=7),
+    dict(region_sharing=False, store="host"), dict(codec=7), dict(codec="trunc16", rate_bits=8),
+    dict(codec="zfp", rate_bits=33), dict(codec="zfp", rate_bits=0),
 ])
 def test_config_errors(kw):
     with pytest.raises(oocs.OocsError) as e:
@@ -71,6 +72,12 @@ def test_encoded_bytes_fixed_rate_law():
     assert oocs.oocs_encoded_bytes(c16, 4) * 2 == oocs.oocs_encoded_bytes(c_id, 4) == 4 * ax * ax * 4
     for r in (8, 12, 24):
         assert oocs.oocs_encoded_bytes(cfg(rate_bits=r), 8) == 8 * ax * ax * r // 8
+        assert oocs.oocs_encoded_bytes(cfg(codec="zfp", rate_bits=r), 8) == 8 * ax * ax * r // 8
+    # Truncate-16: raw bf16 planes, the same bytes as rate-16 BlockQuant
+    assert oocs.oocs_encoded_bytes(cfg(codec="trunc16", rate_bits=16), 4) == oocs.oocs_encoded_bytes(c16, 4)
+    for codec, r in (("trunc16", 16), ("zfp", 12)):
+        assert oocs.oocs_encoded_bytes(cfg(codec=codec, rate_bits=r), 12) == 12 * oracle.plane_bytes(
+            ax, ax, {"trunc16": 3, "zfp": 2}[codec], r)
 
 
 def _geo(c, blocks):
@@ -87,7 +94,7 @@ def _check(c, steps):
 
 
 MODES = [("swb", "blockquant"), ("dwb", "blockquant"), ("compress", "blockquant"), ("baseline", "identity"),
-         ("swb", "identity")]
+         ("swb", "identity"), ("swb", "trunc16")]
 
 
 @pytest.mark.parametrize("sched", ["alg1", "dag", "dag_func"])

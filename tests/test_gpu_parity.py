@@ -143,10 +143,11 @@ def test_stencil_step_within_1e6(nx, ny, nz):
 
 # ----------------------------------------------------------------------------- out-of-core runs
 def make_plan(nx, ny, nz, n, k, codec="blockquant", rate=16, mode="swb", store="host", profile=False,
-              resident_velocity=False, n_lanes=0, schedule="alg1"):
+              resident_velocity=False, n_lanes=0, schedule="alg1", executor="dispatch"):
     c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, codec=codec,
                          rate_bits=rate, mode=mode, store=store, profile=profile,
-                         resident_velocity=resident_velocity, n_lanes=n_lanes, schedule=schedule)
+                         resident_velocity=resident_velocity, n_lanes=n_lanes, schedule=schedule,
+                         executor=executor)
     return oocs.Plan(c)
 
 
@@ -213,9 +214,12 @@ def test_lossy_modes_are_bitwise_identical(rate):
                 ("swb", "host", True, 0, "alg1"), ("swb", "host", False, 4, "alg1"), ("dwb", "host", True, 2, "alg1"),
                 ("swb", "host", False, 0, "dag"), ("swb", "host", False, 0, "dag_func"),
                 ("compress", "host", True, 4, "dag_func")]
-    for mode, store, resident, lanes, sched in variants:
+    # the same schedules replayed onto streams (one per lane, Alg. 1 literally / copy + kernel per lane)
+    # instead of the host dispatcher
+    variants += [v + (ex,) for ex in ("single", "split") for v in variants[:4] + variants[6:8]]
+    for mode, store, resident, lanes, sched, *ex in variants:
         pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store, resident_velocity=resident,
-                       n_lanes=lanes, schedule=sched)
+                       n_lanes=lanes, schedule=sched, executor=ex[0] if ex else "dispatch")
         load_fields(pl, vel, p0)
         pl.run(6)
         outs.append((pl.read_raw(1, 0, az), pl.read_raw(2, 0, az)))

@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=4096)
     ap.add_argument("--ks", default="1,4")
     ap.add_argument("--rates", default="8,12,16,24")
-    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp"])
+    ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp", "trunc16"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_accuracy.json"))
     a = ap.parse_args()
     n, nb = a.n, a.nb
