@@ -53,6 +53,18 @@ struct Xpose {
 
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 
+// (float)code + 0.5f without the quarter-rate I2F: 2^23 + code is the bit pattern 0x4B000000 | code
+// (code < 2^23), and subtracting 2^23 - 0.5 (representable) is exact (Sterbenz)
+__device__ __forceinline__ float bin_centre(uint32_t code) {
+    return __fsub_rn(__uint_as_float(0x4B000000u | code), 8388607.5f);
+}
+// floor(y) for 0 <= y, without the quarter-rate F2I: y + 2^23 rounded down is 2^23 + floor(y) while
+// y < 2^23; beyond, the result is >= 2^23 > every code maximum (2^q - 1, q <= 23), so the caller's
+// clamp gives the same code as min(cmax, floor(y))
+__device__ __forceinline__ uint32_t floor_code(float y) {
+    return __float_as_uint(__fadd_rd(y, 0x1p23f)) - 0x4B000000u;
+}
+
 // Warp task = one 128-byte line segment of 16 rows (4 y x 4 z) of a
 // 4-plane slab: the blocks bx in [max(0,8L-7), min(nbx-1,8L)] whose columns
 // lie in line L (column of x is x + 28, block bx covers x in [4bx, 4bx+4)).
@@ -132,10 +144,8 @@ bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int n
         for (int u = 0; u < 4; ++u) {
             const int r = r0 + 4 * u;
             const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
-            const float4 v = make_float4(__fmaf_rn(__fadd_rn(__uint2float_rn(c.x), 0.5f), step, mn),
-                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.y), 0.5f), step, mn),
-                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.z), 0.5f), step, mn),
-                                         __fmaf_rn(__fadd_rn(__uint2float_rn(c.w), 0.5f), step, mn));
+            const float4 v = make_float4(__fmaf_rn(bin_centre(c.x), step, mn), __fmaf_rn(bin_centre(c.y), step, mn),
+                                         __fmaf_rn(bin_centre(c.z), step, mn), __fmaf_rn(bin_centre(c.w), step, mn));
             __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch), v);
         }
     }
@@ -182,7 +192,7 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     const float scale = small ? 0.f : __fdiv_rn(pow2f(q), range);
     const uint32_t cmax = (1u << q) - 1u;
     auto code = [&](float x) -> uint32_t {
-        return small ? 0u : min(cmax, __float2uint_rd(__fmul_rn(__fsub_rn(x, mn), scale)));
+        return small ? 0u : min(cmax, floor_code(__fmul_rn(__fsub_rn(x, mn), scale)));
     };
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -805,6 +815,31 @@ struct BitReader {
     __device__ __forceinline__ uint32_t get1() { return (uint32_t)get(1); }
 };
 
+// LSB-first reader with a two-word window: the next 64 bits are always one funnel shift away, so a
+// read of m <= 64 bits is a shift, a mask and an advance (bits past the record read as zeros)
+struct BitWin {
+    const uint64_t *in, *end;  // next word to load, end of the record
+    uint64_t lo, hi;           // current word, next word
+    int off;                   // bits of lo already consumed (0..63)
+    __device__ __forceinline__ void init(const uint64_t *p, int words) {
+        end = p + words;
+        lo = __ldg(p);
+        hi = words > 1 ? __ldg(p + 1) : 0;
+        in = p + 2;
+        off = 0;
+    }
+    __device__ __forceinline__ uint64_t peek64() const { return off ? (lo >> off) | (hi << (64 - off)) : lo; }
+    __device__ __forceinline__ void skip(int m) {  // 0 <= m <= 64
+        off += m;
+        if (off >= 64) {
+            off -= 64;
+            lo = hi;
+            hi = in < end ? __ldg(in) : 0;
+            ++in;
+        }
+    }
+};
+
 __device__ __forceinline__ uint32_t zfp_int2uint(int32_t x) { return ((uint32_t)x + 0xaaaaaaaau) ^ 0xaaaaaaaau; }
 __device__ __forceinline__ int32_t zfp_uint2int(uint32_t x) { return (int32_t)((x ^ 0xaaaaaaaau) - 0xaaaaaaaau); }
 
@@ -883,18 +918,20 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
             // group test bit, then the zeros up to the next 1 and that 1 (implied at position 63)
             while (n < 64 && bits > 0) {
                 bits--;
-                bw.put1(plane != 0);
-                if (!plane) break;
+                if (!plane) {  // group test 0
+                    bw.put(0, 1);
+                    break;
+                }
                 const int z = __ffsll((long long)plane) - 1, zmax = 63 - n;
                 const int len = z < zmax ? z + 1 : zmax;  // bits the zfp loop would write
-                if (len <= bits) {
-                    bw.put(z < zmax ? (uint64_t)1 << z : 0, len);
+                if (len <= bits) {  // group bit 1, z zeros and a 1 (implied when n reaches 63): one put
+                    bw.put(1u | (z < zmax ? (uint64_t)2 << z : 0), len + 1);
                     bits -= len;
                     const int adv = z < zmax ? z + 1 : zmax + 1;
                     n += adv;
                     plane = adv >= 64 ? 0 : plane >> adv;
                 } else {  // budget ends inside the zero run
-                    bw.put(0, bits);
+                    bw.put(1u, bits + 1);
                     n += bits + 1;
                     plane = 0;
                     bits = 0;
@@ -917,13 +954,16 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
     if (t >= (int64_t)nbx * nby) return;
     const int bx = (int)(t % nbx), by = (int)(t / nbx), bz = blockIdx.y;
     const uint64_t *rec = src + ((int64_t)(bz * nby + by) * nbx + bx) * rate;
-    BitReader br{rec, 0, 0};
+    BitWin br;
+    br.init(rec, rate);
     float x[64];
-    if (!br.get1()) {
+    const uint64_t head = br.peek64();
+    if (!(head & 1u)) {
 #pragma unroll
         for (int j = 0; j < 64; ++j) x[j] = 0.f;
     } else {
-        const int emax = (int)br.get(8) - 127;
+        const int emax = (int)((head >> 1) & 0xFFu) - 127;
+        br.skip(9);
 #pragma unroll
         for (int k = 0; k < 32; ++k) zs_planes[k][threadIdx.x] = 0;
         int bits = 64 * rate - 9;
@@ -931,27 +971,27 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
 #pragma unroll 1
         for (int k = 31; k >= 0; --k) {
             if (bits <= 0) break;
+            // the first n coefficients (already significant) are sent verbatim
             const int m = min(n, bits);
             bits -= m;
-            uint64_t plane = br.get(m);
+            uint64_t plane = m == 0 ? 0 : m == 64 ? br.peek64() : br.peek64() & (((uint64_t)1 << m) - 1);
+            br.skip(m);
+            // then per newly significant coefficient: group-test bit 1, zeros, a 1 (implied at 63)
             while (n < 64 && bits > 0) {
                 bits--;
-                if (!br.get1()) break;
+                const uint64_t w = br.peek64();
+                if (!(w & 1u)) {  // group test 0: nothing more in this plane
+                    br.skip(1);
+                    break;
+                }
                 const int avail = min(63 - n, bits);  // zeros the zfp loop may read before stopping
-                int z = avail;
-                if (avail > 0) {
-                    const uint64_t look = br.peek(avail);
-                    if (look) z = __ffsll((long long)look) - 1;
-                }
-                if (z < avail) {  // a 1 at position n + z
-                    br.skip(z + 1);
-                    bits -= z + 1;
-                } else {          // n reached 63 (its 1 is implied) or the budget ended
-                    br.skip(avail);
-                    bits -= avail;
-                }
+                const uint64_t t = w >> 1;
+                const int z = min(t ? __ffsll((long long)t) - 1 : 64, avail);  // the next 1, or none in reach
+                const int used = z < avail ? z + 1 : avail;  // run of zeros (+ its terminating 1)
+                br.skip(1 + used);
+                bits -= used;
                 n += z;
-                plane += (uint64_t)1 << n;
+                plane |= (uint64_t)1 << n;
                 n++;
             }
             zs_planes[k][threadIdx.x] = plane;
@@ -970,9 +1010,15 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
 #pragma unroll
         for (int i = 0; i < 64; ++i) ib[P.p[i]] = zfp_uint2int(pl[i]);
         zfp_inv_xform(ib);
-        const double sc = ldexp(1.0, emax - 30);
+        if (emax >= -96) {  // 2^(emax-30) is a normal float: one fp32 product = the exact product rounded once
+            const float sc = __int_as_float((127 + emax - 30) << 23);
 #pragma unroll
-        for (int j = 0; j < 64; ++j) x[j] = (float)((double)__int2float_rn(ib[j]) * sc);
+            for (int j = 0; j < 64; ++j) x[j] = __fmul_rn(__int2float_rn(ib[j]), sc);
+        } else {
+            const double sc = ldexp(1.0, emax - 30);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) x[j] = (float)((double)__int2float_rn(ib[j]) * sc);
+        }
     }
     float *d0 = dst + (int64_t)(4 * bz) * pstride + (int64_t)(4 * by) * pitch + XOFF + 4 * bx;
 #pragma unroll

@@ -10,8 +10,11 @@ import paper_2204_11315_b200 as oocs  # noqa: E402
 import synth  # noqa: E402
 
 nx, ny, nz, nb, k, T, rate = bench.WORKLOADS[os.environ.get("WL", "c2")]
+codec = sys.argv[sys.argv.index("--codec") + 1] if "--codec" in sys.argv else "blockquant"
+if codec == "trunc16":
+    rate = 16
 c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, rate_bits=rate,
-                     mode="swb", store="device")
+                     mode="swb", store="device", codec=codec)
 pl = oocs.Plan(c)
 bench.load_state(pl, nx, ny, nz, 0)
 pl.run(k)
