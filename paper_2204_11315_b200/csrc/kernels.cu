@@ -786,35 +786,6 @@ struct BitWriter {
     }
 };
 
-struct BitReader {
-    const uint64_t *in;
-    uint64_t cur;  // the nb unconsumed bits, LSB first (higher bits zero)
-    int nb;
-    __device__ __forceinline__ uint64_t peek(int m) const {  // next m bits (1 <= m <= 64), not consumed
-        uint64_t v = cur;
-        if (m > nb) v |= __ldg(in) << nb;  // nb < 64 here
-        return m == 64 ? v : v & (((uint64_t)1 << m) - 1);
-    }
-    __device__ __forceinline__ void skip(int m) {  // consume m bits (0 <= m <= 64)
-        if (m < nb) {
-            cur >>= m;
-            nb -= m;
-        } else {
-            const int r = m - nb;
-            const uint64_t w = __ldg(in++);
-            cur = r == 64 ? 0 : w >> r;
-            nb = 64 - r;
-        }
-    }
-    __device__ __forceinline__ uint64_t get(int m) {
-        if (m == 0) return 0;
-        const uint64_t v = peek(m);
-        skip(m);
-        return v;
-    }
-    __device__ __forceinline__ uint32_t get1() { return (uint32_t)get(1); }
-};
-
 // LSB-first reader with a two-word window: the next 64 bits are always one funnel shift away, so a
 // read of m <= 64 bits is a shift, a mask and an advance (bits past the record read as zeros)
 struct BitWin {

@@ -804,7 +804,10 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
     auto complete = [&](int64_t d) -> bool {
         if (done[d]) return true;
         const cudaError_t e = cudaEventQuery(p->op_done[d]);
-        if (e == cudaSuccess) return done[d] = 1;
+        if (e == cudaSuccess) {
+            done[d] = 1;
+            return true;
+        }
         if (e != cudaErrorNotReady) (void)cudaGetLastError();
         return false;
     };
