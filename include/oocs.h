@@ -268,6 +268,13 @@ oocs_status oocs_encoded_bytes(const oocs_config *cfg, int64_t planes, uint64_t 
  * cudaMalloc failure), OOCS_ERR_HOST_OOM, OOCS_ERR_CUDA. */
 oocs_status oocs_plan_create(const oocs_config *cfg, oocs_plan **out);
 
+/* The same on a caller-owned device arena (SURVEY §8(b) "optional torch-owned arena"): `arena` is device
+ * memory of cfg->device, 256-byte aligned, at least oocs_plan_estimate(cfg).arena_bytes long; the plan
+ * carves its working sets, staging and device store out of it, zeroes it, and never frees it -- the
+ * caller keeps it alive until oocs_destroy.  Errors: as oocs_plan_create, plus OOCS_ERR_CONFIG for a
+ * NULL, short, misaligned or non-device arena. */
+oocs_status oocs_plan_create_in(const oocs_config *cfg, void *arena, uint64_t arena_bytes, oocs_plan **out);
+
 oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info);
 
 /* Install the halo-exchange callback (required when world > 1). */

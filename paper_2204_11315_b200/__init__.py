@@ -121,6 +121,7 @@ def lib():
             "oocs_schedule": ([P(Config), i64, vp, i64, P(i64)], i32),
             "oocs_encoded_bytes": ([P(Config), i64, P(u64)], i32),
             "oocs_plan_create": ([P(Config), P(vp)], i32),
+            "oocs_plan_create_in": ([P(Config), vp, u64, P(vp)], i32),
             "oocs_plan_query": ([vp, P(PlanInfo)], i32),
             "oocs_plan_estimate": ([P(Config), P(PlanInfo)], i32),
             "oocs_set_exchange": ([vp, EXCHANGE_FN, vp], i32),
@@ -213,6 +214,13 @@ def oocs_plan_create(cfg: Config):
     return h
 
 
+def oocs_plan_create_in(cfg: Config, arena_ptr: int, arena_bytes: int):
+    h = vp()
+    _check(lib().oocs_plan_create_in(ctypes.byref(cfg), arena_ptr, arena_bytes, ctypes.byref(h)),
+           "oocs_plan_create_in")
+    return h
+
+
 def oocs_plan_query(h) -> PlanInfo:
     info = PlanInfo()
     _check(lib().oocs_plan_query(h, ctypes.byref(info)), "oocs_plan_query")
@@ -288,9 +296,13 @@ class Plan:
     """Convenience owner of an oocs_plan handle (same calls as the C ABI)."""
     cfg: Config
     handle: object = None
+    arena: object = None  # optional caller-owned device buffer (e.g. a torch uint8 tensor) to carve from
 
     def __post_init__(self):
-        self.handle = oocs_plan_create(self.cfg)
+        if self.arena is not None:
+            self.handle = oocs_plan_create_in(self.cfg, self.arena.data_ptr(), self.arena.numel() * self.arena.element_size())
+        else:
+            self.handle = oocs_plan_create(self.cfg)
         self.info = oocs_plan_query(self.handle)
         self._cb = None
 

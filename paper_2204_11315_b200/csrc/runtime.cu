@@ -324,7 +324,7 @@ static void fill_info(const Geometry &g, const Sizes &z, oocs_plan_info *info) {
     info->n_lanes = g.lanes;
 }
 
-static oocs_status create(const oocs_config *cfg, Plan **out) {
+static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = nullptr, uint64_t ext_bytes = 0) {
     *out = nullptr;
     oocs_plan *p = new (std::nothrow) oocs_plan();
     if (!p) return OOCS_ERR_HOST_OOM;
@@ -356,15 +356,35 @@ static oocs_status create(const oocs_config *cfg, Plan **out) {
         delete p;
         return OOCS_ERR_DEVICE_OOM;
     }
-    cudaError_t ce = cudaMalloc((void **)&p->arena.base, total);
-    if (ce != cudaSuccess) {
-        cudaGetLastError();
-        set_error(std::string("cudaMalloc of the device arena failed: ") + cudaGetErrorString(ce));
-        delete p;
-        return OOCS_ERR_DEVICE_OOM;
+    cudaError_t ce = cudaSuccess;
+    if (ext_arena) {  // caller-owned device memory (e.g. a torch tensor), kept alive by the caller
+        if (ext_bytes < total || (reinterpret_cast<uintptr_t>(ext_arena) & 255)) {
+            set_error("external arena too small (need " + std::to_string(total) + " B, see oocs_plan_estimate) or "
+                      "not 256-byte aligned");
+            delete p;
+            return OOCS_ERR_CONFIG;
+        }
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, ext_arena) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+            pa.device != g.cfg.device) {
+            cudaGetLastError();
+            set_error("external arena is not device memory of the plan's device");
+            delete p;
+            return OOCS_ERR_CONFIG;
+        }
+        p->arena.base = static_cast<char *>(ext_arena);
+        p->arena.owned = false;
+    } else {
+        ce = cudaMalloc((void **)&p->arena.base, total);
+        if (ce != cudaSuccess) {
+            cudaGetLastError();
+            set_error(std::string("cudaMalloc of the device arena failed: ") + cudaGetErrorString(ce));
+            delete p;
+            return OOCS_ERR_DEVICE_OOM;
+        }
+        p->arena.owned = true;
     }
     p->arena.cap = total;
-    p->arena.owned = true;
     for (int s = 0; s < g.n_ws; ++s)
         for (int a = 0; a < N_ARRAYS; ++a) p->ws[s][a] = (float *)p->arena.take(ws_array);
     if (codec_staging)
@@ -1071,6 +1091,18 @@ oocs_status oocs_plan_create(const oocs_config *cfg, oocs_plan **out) {
     *out = nullptr;
     Plan *p = nullptr;
     oocs_status st = create(cfg, &p);
+    if (st == OOCS_OK) *out = static_cast<oocs_plan *>(p);
+    return st;
+}
+
+oocs_status oocs_plan_create_in(const oocs_config *cfg, void *arena, uint64_t arena_bytes, oocs_plan **out) {
+    if (!out || !arena) {
+        set_error("out or arena is NULL");
+        return OOCS_ERR_CONFIG;
+    }
+    *out = nullptr;
+    Plan *p = nullptr;
+    oocs_status st = create(cfg, &p, arena, arena_bytes);
     if (st == OOCS_OK) *out = static_cast<oocs_plan *>(p);
     return st;
 }

@@ -225,3 +225,10 @@ def test_dag_schedule_derives_no_more_waits_than_alg1(mode):
     idx = [i for i, o in enumerate(d) if o["kind"] == "WAIT"]
     caught = sum(bool(sc.violations(d[:i] + d[i + 1:], blocks, geo, limit=1)) for i in idx)
     assert caught >= len(idx) * 3 // 4  # (almost) every derived wait is load-bearing
+
+
+def test_create_in_rejects_null_arena_without_a_gpu():
+    # argument checks come before any CUDA call, so this runs on a CPU-only box
+    with pytest.raises(oocs.OocsError) as e:
+        oocs.oocs_plan_create_in(cfg(), 0, 1 << 20)
+    assert e.value.status == 2
