@@ -168,6 +168,8 @@ typedef struct {
     uint64_t alg_bytes[3];          /* algorithmic HBM bytes per kind */
     int32_t data_error;             /* 1 if the encoder saw NaN/Inf/|x|>=2^126 */
     int32_t reserved;
+    double busy_ms[4];              /* OOCS_FLAG_TIMELINE: busy time (union of op spans) of the H2D copies, the
+                                     * D2H copies, the kernels and the exchange; 0 without the flag */
 } oocs_stats;
 
 /* One entry of the decomposition table (interior plane coordinates,
@@ -344,6 +346,10 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
 /* ---- misc -------------------------------------------------------------- */
 const char *oocs_last_error(void);
 int32_t oocs_abi_version(void);
+
+/* sizeof of the ABI structs, for bindings to check their mirrors: out[0..5] = oocs_config, oocs_stats,
+ * oocs_plan_info, oocs_block, oocs_op, oocs_span.  Host-only. */
+void oocs_abi_sizes(int64_t out[6]);
 
 #ifdef __cplusplus
 }

@@ -69,7 +69,8 @@ class PlanInfo(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("wall_ms", f64), ("kernel_ms", f64 * 3), ("kernel_launches", i64 * 3), ("bytes_h2d", u64),
                 ("bytes_d2h", u64), ("bytes_d2d", u64), ("bytes_exchange", u64), ("cell_updates", u64),
-                ("cell_updates_computed", u64), ("alg_bytes", u64 * 3), ("data_error", i32), ("reserved", i32)]
+                ("cell_updates_computed", u64), ("alg_bytes", u64 * 3), ("data_error", i32), ("reserved", i32),
+                ("busy_ms", f64 * 4)]
 
     def as_dict(self):
         return {
@@ -137,6 +138,7 @@ def lib():
             "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, vp], i32),
             "oocs_last_error": ([], ctypes.c_char_p),
             "oocs_abi_version": ([], i32),
+            "oocs_abi_sizes": ([vp], None),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

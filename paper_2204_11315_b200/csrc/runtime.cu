@@ -943,6 +943,31 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
         p->spans[i].start_ms = a;
         p->spans[i].end_ms = b;
     }
+    {
+        // busy time per engine = length of the union of its spans
+        std::vector<std::pair<double, double>> iv[4];
+        for (const oocs_span &s : p->spans) {
+            const int e = s.kind == OOCS_OP_H2D ? 0 : s.kind == OOCS_OP_D2H ? 1
+                        : (s.kind == OOCS_OP_DECODE || s.kind == OOCS_OP_STEP || s.kind == OOCS_OP_ENCODE) ? 2
+                        : s.kind == OOCS_OP_EXCHANGE ? 3 : -1;
+            if (e >= 0) iv[e].emplace_back(s.start_ms, s.end_ms);
+        }
+        for (int e = 0; e < 4; ++e) {
+            std::sort(iv[e].begin(), iv[e].end());
+            double tot = 0, lo = 0, hi = -1;
+            for (auto &x : iv[e]) {
+                if (x.first > hi) {
+                    if (hi > lo) tot += hi - lo;
+                    lo = x.first;
+                    hi = x.second;
+                } else {
+                    hi = std::max(hi, x.second);
+                }
+            }
+            if (hi > lo) tot += hi - lo;
+            stats.busy_ms[e] = tot;
+        }
+    }
     int herr = 0;
     CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     stats.data_error = herr;
@@ -1230,5 +1255,14 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
 
 const char *oocs_last_error(void) { return g_last_error.c_str(); }
 int32_t oocs_abi_version(void) { return OOCS_ABI_VERSION; }
+
+void oocs_abi_sizes(int64_t out[6]) {
+    out[0] = sizeof(oocs_config);
+    out[1] = sizeof(oocs_stats);
+    out[2] = sizeof(oocs_plan_info);
+    out[3] = sizeof(oocs_block);
+    out[4] = sizeof(oocs_op);
+    out[5] = sizeof(oocs_span);
+}
 
 }  // extern "C"

@@ -232,3 +232,10 @@ def test_create_in_rejects_null_arena_without_a_gpu():
     with pytest.raises(oocs.OocsError) as e:
         oocs.oocs_plan_create_in(cfg(), 0, 1 << 20)
     assert e.value.status == 2
+
+
+def test_binding_structs_mirror_the_header():
+    out = (ctypes.c_int64 * 6)()
+    oocs.lib().oocs_abi_sizes(out)
+    mine = [ctypes.sizeof(t) for t in (oocs.Config, oocs.Stats, oocs.PlanInfo, oocs.Block, oocs.Op, oocs.Span)]
+    assert list(out) == mine

@@ -59,6 +59,18 @@ def test_timeline_spans_and_orderings(store, sched, executor):
             for j in (i, i + 1):
                 if j < n:
                     assert by[("H2D", g, 0)]["start_ms"] >= by[("D2H", g - n + (j - i), 0)]["end_ms"] - EPS
+    # engine busy times in the stats = union of the spans
+    for e, kinds in enumerate((("H2D",), ("D2H",), ("DECODE", "STEP", "ENCODE"))):
+        iv = sorted((s["start_ms"], s["end_ms"]) for s in spans if s["kind"] in kinds)
+        tot, lo, hi = 0.0, 0.0, -1.0
+        for a, b in iv:
+            if a > hi:
+                tot += max(hi - lo, 0.0)
+                lo, hi = a, b
+            else:
+                hi = max(hi, b)
+        tot += max(hi - lo, 0.0)
+        assert abs(st.busy_ms[e] - tot) < 1e-3 * max(tot, 1.0)
     # the flag off: no spans
     pl.close()
     c2 = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, rate_bits=16,
