@@ -58,12 +58,7 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 __device__ __forceinline__ float bin_centre(uint32_t code) {
     return __fsub_rn(__uint_as_float(0x4B000000u | code), 8388607.5f);
 }
-// floor(y) for 0 <= y, without the quarter-rate F2I: y + 2^23 rounded down is 2^23 + floor(y) while
-// y < 2^23; beyond, the result is >= 2^23 > every code maximum (2^q - 1, q <= 23), so the caller's
-// clamp gives the same code as min(cmax, floor(y))
-__device__ __forceinline__ uint32_t floor_code(float y) {
-    return __float_as_uint(__fadd_rd(y, 0x1p23f)) - 0x4B000000u;
-}
+
 
 // Warp task = one 128-byte line segment of 16 rows (4 y x 4 z) of a
 // 4-plane slab: the blocks bx in [max(0,8L-7), min(nbx-1,8L)] whose columns
@@ -168,7 +163,8 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     const int q = QT ? QT : q_rt;
     const int ib = lane & 7, r0 = lane >> 3;
     float mn = v[0].x, mx = v[0].x;
-    bool nan = false;
+    // x * 0 is NaN exactly for NaN and Inf: one FMA per value flags them (fminf/fmaxf skip NaNs)
+    float nz[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
@@ -176,9 +172,11 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
         for (int c = 0; c < 4; ++c) {
             mn = fminf(mn, e[c]);
             mx = fmaxf(mx, e[c]);
-            nan |= e[c] != e[c];
+            nz[c] = __fmaf_rn(e[c], 0.f, nz[c]);
         }
     }
+    const float nzs = __fadd_rn(__fadd_rn(nz[0], nz[1]), __fadd_rn(nz[2], nz[3]));
+    const bool nan = nzs != nzs;
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 8));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
@@ -191,8 +189,14 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     const bool small = !(step >= 0x1p-126f);
     const float scale = small ? 0.f : __fdiv_rn(pow2f(q), range);
     const uint32_t cmax = (1u << q) - 1u;
+    // code = min(cmax, floor(y)), y = (x - mn) * scale >= 0, without the quarter-rate F2I: y + 2^23
+    // rounded down is the pattern of 2^23 + floor(y) while y < 2^23, and beyond it is >= 2^23 + 2^23 >
+    // every clamp, so the min gives the same code.  When q <= 16 the pattern itself (2^23 + code) is
+    // kept: the transpose below only uses its low 16 bits, which are the code's.  scale = 0 (a
+    // (near-)constant block) makes every code 0
     auto code = [&](float x) -> uint32_t {
-        return small ? 0u : min(cmax, floor_code(__fmul_rn(__fsub_rn(x, mn), scale)));
+        const uint32_t bits = __float_as_uint(__fadd_rd(__fmul_rn(__fsub_rn(x, mn), scale), 0x1p23f));
+        return TWO ? min(cmax, bits - 0x4B000000u) : min(cmax + 0x4B000000u, bits);
     };
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
