@@ -376,13 +376,15 @@ static dim3 tr16_grid(int64_t plane8, int64_t planes) {
 // queue indexed at compile time (the plane loop is unrolled by 9), x/y
 // neighbours come from the ring with 64-bit shared loads.
 // ---------------------------------------------------------------------------
-// TY = tile rows (16: 256 threads, 2 CTAs per SM).  The p_curr ring has 7 slots: at plane z it holds
-// the x/y-neighbour plane z, the queue-feed plane z+4 and the two planes in flight (z+5, z+6).
+// TY = tile rows (16: 256 threads, 2 CTAs per SM).  The p_curr ring needs 7 slots: at plane z it holds
+// the x/y-neighbour plane z, the queue-feed plane z+4 and the two planes in flight (z+5, z+6).  The
+// plain step uses 9, one per unrolled plane, so every slot index is a compile-time constant; the
+// encoding variant, whose slab staging needs the shared memory, uses 7 with runtime slots.
 template <int TY>
 struct S2T {
     static constexpr int TX = 64, THREADS = 16 * TY, CTAS = TY == 16 ? 2 : 1;
     static constexpr int PW = TX + 2 * R, PH = TY + 2 * R;  // p_curr box with the star halo
-    static constexpr int NS = 7, NB = 3, D = 2;             // ring slots, p_prev/v stages, prefetch distance
+    static constexpr int NB = 3, D = 2;                     // p_prev/v stages, prefetch distance
     static constexpr uint32_t PBYTES = PW * PH * 4, TBYTES = TX * TY * 4;
 };
 // ENC selects the stencil variant: 0 = plain step; otherwise the last step of a sweep that also
@@ -390,9 +392,12 @@ struct S2T {
 // one-word q <= 16, generic two-word q > 16), keeping the kernel's instruction footprint small
 enum { ENC_NONE = 0, ENC_Q15 = 1, ENC_ONE = 2, ENC_TWO = 3 };
 
+template <int ENC>
+__host__ __device__ constexpr int s2_ring() { return ENC ? 7 : 9; }
+
 template <int TY, int ENC>
 struct S2Smem {
-    float p[7][TY + 2 * R][64 + 2 * R];
+    float p[s2_ring<ENC>()][TY + 2 * R][64 + 2 * R];
     float pp[3][TY][64];
     float v[3][TY][64];
     // ENC: the 4-plane slab being completed, [prev/curr][plane][row][col]; the encode phase reuses it
@@ -400,7 +405,7 @@ struct S2Smem {
     float stage[ENC ? 2 : 1][ENC ? 4 : 1][ENC ? TY : 1][ENC ? 64 : 4];
     unsigned long long bar[4];
 };
-constexpr int S2_TX = 64, S2_NS = 7, S2_NB = 3, S2_D = 2;
+constexpr int S2_TX = 64, S2_NB = 3, S2_D = 2;
 
 // coefficients of d2/dx2, order 8 (Q1): 8/5, -1/5, 8/315, -1/560
 #define C1 1.6f
@@ -456,15 +461,16 @@ __device__ __noinline__ void s2_encode_slab(S2Smem<TY, ENC> &S, const StepArgs &
 template <int OFF, int TY, int ENC>
 __device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *mP, const CUtensorMap *mPP,
                                          const CUtensorMap *mV, const StepArgs &a, int z, int zs, int ze,
-                                         int x0, int y0, float (&q)[9][4], uint32_t &ph, bool okr0,
+                                         int x0, int y0, float2 (&q)[9][2], uint32_t &ph, bool okr0,
                                          bool okr1, int64_t g0) {
     if (z >= ze) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // every thread is done with plane z-1: its ring slots may be refilled
-    // ring slot of plane P is (P - zs + 4) mod 7
-    const int rel = z - zs;
+    // ring slot of plane P is (P - zs + 4) mod NS (NS = 9: OFF + 4 mod 9, known at compile time)
+    constexpr int NS = s2_ring<ENC>();
+    const int rel = NS == 9 ? OFF : z - zs;
     if (tid == 0 && z + S2_D < ze) {
-        const int ps = (rel + 4 + S2_D + R) % S2_NS;  // slot of plane z+D+4 (previously plane z-1)
+        const int ps = (rel + 4 + S2_D + R) % NS;  // slot of plane z+D+4 (previously plane z+D+4-NS)
         constexpr int st = (OFF + S2_D) % S2_NB;     // stage of plane z+D
         unsigned long long *bar = &S.bar[st];
         mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
@@ -475,82 +481,71 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *
     constexpr int st = OFF % S2_NB;
     mbar_wait(&S.bar[st], (ph >> st) & 1u);
     ph ^= 1u << st;
-    const int sz = (rel + 4) % S2_NS, sz4 = (rel + 4 + R) % S2_NS;
+    const int sz = (rel + 4) % NS, sz4 = (rel + 4 + R) % NS;
     const int cx = 2 * lane, cy = 2 * warp;
     // feed the queue with plane z+4 (own cells)
-    {
-        const float2 a0 = *reinterpret_cast<const float2 *>(&S.p[sz4][R + cy][R + cx]);
-        const float2 a1 = *reinterpret_cast<const float2 *>(&S.p[sz4][R + cy + 1][R + cx]);
-        q[(OFF + 8) % 9][0] = a0.x;
-        q[(OFF + 8) % 9][1] = a0.y;
-        q[(OFF + 8) % 9][2] = a1.x;
-        q[(OFF + 8) % 9][3] = a1.y;
-    }
+    q[(OFF + 8) % 9][0] = *reinterpret_cast<const float2 *>(&S.p[sz4][R + cy][R + cx]);
+    q[(OFF + 8) % 9][1] = *reinterpret_cast<const float2 *>(&S.p[sz4][R + cy + 1][R + cx]);
     const float(*P)[S2T<TY>::PW] = S.p[sz];
     // y neighbours: rows cy..cy+3 and cy+6..cy+9 of the box at columns cx+4, cx+5
     float2 yr[10];
 #pragma unroll
     for (int m = 0; m < 10; ++m)
         if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&P[cy + m][R + cx]);
-    yr[4] = make_float2(q[(OFF + 4) % 9][0], q[(OFF + 4) % 9][1]);
-    yr[5] = make_float2(q[(OFF + 4) % 9][2], q[(OFF + 4) % 9][3]);
+    yr[4] = q[(OFF + 4) % 9][0];
+    yr[5] = q[(OFF + 4) % 9][1];
     const float2 pp0 = *reinterpret_cast<const float2 *>(&S.pp[st][cy][cx]);
     const float2 pp1 = *reinterpret_cast<const float2 *>(&S.pp[st][cy + 1][cx]);
     const float2 v0 = *reinterpret_cast<const float2 *>(&S.v[st][cy][cx]);
     const float2 v1 = *reinterpret_cast<const float2 *>(&S.v[st][cy + 1][cx]);
-    float out[4];
+    // The two x-adjacent cells of a row go through Blackwell's paired fp32 pipe (FADD2 / FMUL2 /
+    // FFMA2): every operation is the same IEEE-rounded scalar operation as before, on both cells at
+    // once, so results are bitwise those of the scalar form below (difference form, x-y-z FMA chain):
+    //   lap = C1((f(x-1)+f(x+1)) - 2f0) + ... ;  p_next = (v dt)^2 lap + (2 f0 - p_prev)
+    const float2 k1 = make_float2(C1, C1), k2 = make_float2(C2, C2), k3 = make_float2(C3, C3),
+                 k4 = make_float2(C4, C4);
+    float2 out[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         const int row = R + cy + r;
         // x neighbours: columns cx..cx+3 and cx+6..cx+9 (centres cx+4, cx+5 come from the queue)
-        float xr[10];
         const float2 xa = *reinterpret_cast<const float2 *>(&P[row][cx]);
         const float2 xb = *reinterpret_cast<const float2 *>(&P[row][cx + 2]);
         const float2 xc = *reinterpret_cast<const float2 *>(&P[row][cx + 6]);
         const float2 xd = *reinterpret_cast<const float2 *>(&P[row][cx + 8]);
-        xr[0] = xa.x; xr[1] = xa.y; xr[2] = xb.x; xr[3] = xb.y;
-        xr[4] = q[(OFF + 4) % 9][2 * r];
-        xr[5] = q[(OFF + 4) % 9][2 * r + 1];
-        xr[6] = xc.x; xr[7] = xc.y; xr[8] = xd.x; xr[9] = xd.y;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int ci = 2 * r + i;
-            const float f0 = q[(OFF + 4) % 9][ci];
-            const float f2 = __fadd_rn(f0, f0);
-            const int cxi = 4 + i;  // column of the centre in xr
-            const int ryi = 4 + r;  // row of the centre in yr
-            auto yv = [&](int m) { return i ? yr[m].y : yr[m].x; };
-            float lap = __fmul_rn(C1, __fsub_rn(__fadd_rn(xr[cxi - 1], xr[cxi + 1]), f2));
-            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(xr[cxi - 2], xr[cxi + 2]), f2), lap);
-            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(xr[cxi - 3], xr[cxi + 3]), f2), lap);
-            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(xr[cxi - 4], xr[cxi + 4]), f2), lap);
-            lap = __fmaf_rn(C1, __fsub_rn(__fadd_rn(yv(ryi - 1), yv(ryi + 1)), f2), lap);
-            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(yv(ryi - 2), yv(ryi + 2)), f2), lap);
-            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(yv(ryi - 3), yv(ryi + 3)), f2), lap);
-            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(yv(ryi - 4), yv(ryi + 4)), f2), lap);
-            lap = __fmaf_rn(C1, __fsub_rn(__fadd_rn(q[(OFF + 3) % 9][ci], q[(OFF + 5) % 9][ci]), f2), lap);
-            lap = __fmaf_rn(C2, __fsub_rn(__fadd_rn(q[(OFF + 2) % 9][ci], q[(OFF + 6) % 9][ci]), f2), lap);
-            lap = __fmaf_rn(C3, __fsub_rn(__fadd_rn(q[(OFF + 1) % 9][ci], q[(OFF + 7) % 9][ci]), f2), lap);
-            lap = __fmaf_rn(C4, __fsub_rn(__fadd_rn(q[(OFF + 0) % 9][ci], q[(OFF + 8) % 9][ci]), f2), lap);
-            const float vv = r ? (i ? v1.y : v1.x) : (i ? v0.y : v0.x);
-            const float pv = r ? (i ? pp1.y : pp1.x) : (i ? pp0.y : pp0.x);
-            const float vd = __fmul_rn(vv, a.dt);
-            out[ci] = __fmaf_rn(__fmul_rn(vd, vd), lap, __fsub_rn(f2, pv));
-        }
+        const float2 f0 = q[(OFF + 4) % 9][r];
+        const float2 f2 = __fadd2_rn(f0, f0);
+        const float2 nf2 = make_float2(-f2.x, -f2.y);
+        // (f(-m) + f(+m)) - 2 f0 for both cells
+        auto d = [&](float2 lo, float2 hi) { return __fadd2_rn(__fadd2_rn(lo, hi), nf2); };
+        float2 lap = __fmul2_rn(k1, d(make_float2(xb.y, f0.x), make_float2(f0.y, xc.x)));
+        lap = __ffma2_rn(k2, d(xb, xc), lap);
+        lap = __ffma2_rn(k3, d(make_float2(xa.y, xb.x), make_float2(xc.y, xd.x)), lap);
+        lap = __ffma2_rn(k4, d(xa, xd), lap);
+        lap = __ffma2_rn(k1, d(yr[3 + r], yr[5 + r]), lap);
+        lap = __ffma2_rn(k2, d(yr[2 + r], yr[6 + r]), lap);
+        lap = __ffma2_rn(k3, d(yr[1 + r], yr[7 + r]), lap);
+        lap = __ffma2_rn(k4, d(yr[0 + r], yr[8 + r]), lap);
+        lap = __ffma2_rn(k1, d(q[(OFF + 3) % 9][r], q[(OFF + 5) % 9][r]), lap);
+        lap = __ffma2_rn(k2, d(q[(OFF + 2) % 9][r], q[(OFF + 6) % 9][r]), lap);
+        lap = __ffma2_rn(k3, d(q[(OFF + 1) % 9][r], q[(OFF + 7) % 9][r]), lap);
+        lap = __ffma2_rn(k4, d(q[(OFF + 0) % 9][r], q[(OFF + 8) % 9][r]), lap);
+        const float2 vv = r ? v1 : v0, pv = r ? pp1 : pp0;
+        const float2 vd = __fmul2_rn(vv, make_float2(a.dt, a.dt));
+        out[r] = __ffma2_rn(__fmul2_rn(vd, vd), lap, __fadd2_rn(f2, make_float2(-pv.x, -pv.y)));
     }
     if (!ENC) {
         float *dst = a.pprev + (int64_t)z * a.pstride + g0;
-        if (okr0) __stcs(reinterpret_cast<float2 *>(dst), make_float2(out[0], out[1]));
-        if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), make_float2(out[2], out[3]));
+        if (okr0) __stcs(reinterpret_cast<float2 *>(dst), out[0]);
+        if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), out[1]);
     } else {
         // last step: level k is not written back; (level k-1, level k) of the own cells go to the
         // slab staging, and a completed 4-plane slab is encoded straight into the records
         const int sl = (z - zs) & 3;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            *reinterpret_cast<float2 *>(&S.stage[0][sl][cy + r][cx]) =
-                make_float2(q[(OFF + 4) % 9][2 * r], q[(OFF + 4) % 9][2 * r + 1]);
-            *reinterpret_cast<float2 *>(&S.stage[1][sl][cy + r][cx]) = make_float2(out[2 * r], out[2 * r + 1]);
+            *reinterpret_cast<float2 *>(&S.stage[0][sl][cy + r][cx]) = q[(OFF + 4) % 9][r];
+            *reinterpret_cast<float2 *>(&S.stage[1][sl][cy + r][cx]) = out[r];
         }
         if (sl == 3) s2_encode_slab<TY, ENC>(S, a, x0, y0, z - 3);
     }
@@ -631,28 +626,30 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
         // first D stages (plane z+4 of p_curr, plane z of p_prev and v)
         unsigned long long *pro = &S.bar[S2_NB];
         mbar_expect_tx(pro, 4 * S2T<TY>::PBYTES);
-        for (int i = 0; i < 4; ++i) tma_load_3d(&S.p[(4 + i) % S2_NS][0][0], &mP, XOFF + x0, y0, zs + i, pro);
+        constexpr int NS = s2_ring<ENC>();
+        for (int i = 0; i < 4; ++i) tma_load_3d(&S.p[(4 + i) % NS][0][0], &mP, XOFF + x0, y0, zs + i, pro);
         for (int j = 0; j < S2_D; ++j) {
             const int z = zs + j;
             if (z >= ze) break;
             unsigned long long *bar = &S.bar[j % S2_NB];
             mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
-            tma_load_3d(&S.p[(j + 4 + R) % S2_NS][0][0], &mP, XOFF + x0, y0, z + R, bar);
+            tma_load_3d(&S.p[(j + 4 + R) % NS][0][0], &mP, XOFF + x0, y0, z + R, bar);
             tma_load_3d(&S.pp[j % S2_NB][0][0], &mPP, XOFF + R + x0, R + y0, z, bar);
             tma_load_3d(&S.v[j % S2_NB][0][0], &mV, XOFF + R + x0, R + y0, z, bar);
         }
     }
     // register queue: planes zs-4 .. zs+3 of the own 2x2 cells (index m <-> plane zs-4+m)
-    float q[9][4];
+    float2 q[9][2];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         const float *src = a.pcurr + (int64_t)(zs - R + m) * a.pstride + g0;
         float2 r0 = make_float2(0.f, 0.f), r1 = r0;
         if (okr0) r0 = __ldg(reinterpret_cast<const float2 *>(src));
         if (okr1) r1 = __ldg(reinterpret_cast<const float2 *>(src + a.pitch));
-        q[m][0] = r0.x; q[m][1] = r0.y; q[m][2] = r1.x; q[m][3] = r1.y;
+        q[m][0] = r0;
+        q[m][1] = r1;
     }
-    q[8][0] = q[8][1] = q[8][2] = q[8][3] = 0.f;
+    q[8][0] = q[8][1] = make_float2(0.f, 0.f);
     mbar_wait(&S.bar[S2_NB], 0);
     uint32_t ph = 0;
     for (int zb = zs; zb < ze; zb += 9) {

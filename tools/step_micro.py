@@ -43,3 +43,20 @@ for name, (zlo, zhi), fl in [("152 planes", (R, R + 152), False), ("152 planes, 
     ms = sorted(ts)[len(ts) // 2]
     alg = (zhi - zlo) * nx * ny * 16
     print(f"{name}: median {ms * 1e3:.1f} us, {alg / ms / 1e6:.0f} GB/s algorithmic, min {min(ts) * 1e3:.1f} us")
+
+# sustained: back-to-back launches for ~4 s; per-launch time early vs late (power cap / clocks)
+ts = []
+for i in range(9000):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    launch(R, R + 152)
+    e1.record()
+    ts.append((e0, e1))
+    if len(ts) >= 9000 or (i > 100 and sum(1 for _ in ()) > 0):
+        break
+torch.cuda.synchronize()
+ms = [a.elapsed_time(b) for a, b in ts]
+alg = 152 * nx * ny * 16
+for lo, hi in ((0, 50), (1000, 1050), (4000, 4050), (8900, 8950)):
+    seg = sorted(ms[lo:hi])
+    print(f"sustained launches {lo}-{hi}: median {seg[len(seg) // 2] * 1e3:.1f} us = {alg / seg[len(seg) // 2] / 1e6:.0f} GB/s")
