@@ -55,8 +55,20 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 
 // (float)code + 0.5f without the quarter-rate I2F: 2^23 + code is the bit pattern 0x4B000000 | code
 // (code < 2^23), and subtracting 2^23 - 0.5 (representable) is exact (Sterbenz)
-__device__ __forceinline__ float bin_centre(uint32_t code) {
-    return __fsub_rn(__uint_as_float(0x4B000000u | code), 8388607.5f);
+// (two codes at once, paired fp32)
+__device__ __forceinline__ float2 bin_centre2(uint32_t c0, uint32_t c1) {
+    return __fadd2_rn(make_float2(__uint_as_float(0x4B000000u | c0), __uint_as_float(0x4B000000u | c1)),
+                      make_float2(-8388607.5f, -8388607.5f));
+}
+// paired fp32 add rounded toward -inf (FADD2.RM)
+__device__ __forceinline__ float2 fadd2_rd(float2 a, float2 b) {
+    unsigned long long ua, ub, ur;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(ur) : "l"(ua), "l"(ub));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(ur));
+    return r;
 }
 
 
@@ -139,8 +151,10 @@ bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int n
         for (int u = 0; u < 4; ++u) {
             const int r = r0 + 4 * u;
             const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
-            const float4 v = make_float4(__fmaf_rn(bin_centre(c.x), step, mn), __fmaf_rn(bin_centre(c.y), step, mn),
-                                         __fmaf_rn(bin_centre(c.z), step, mn), __fmaf_rn(bin_centre(c.w), step, mn));
+            // two values per paired-fp32 op (same IEEE operations as the scalar fma(code + 0.5, step, mn))
+            const float2 s2 = make_float2(step, step), m2 = make_float2(mn, mn);
+            const float2 lo = __ffma2_rn(bin_centre2(c.x, c.y), s2, m2), hi = __ffma2_rn(bin_centre2(c.z, c.w), s2, m2);
+            const float4 v = make_float4(lo.x, lo.y, hi.x, hi.y);
             __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch), v);
         }
     }
@@ -163,8 +177,9 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     const int q = QT ? QT : q_rt;
     const int ib = lane & 7, r0 = lane >> 3;
     float mn = v[0].x, mx = v[0].x;
-    // x * 0 is NaN exactly for NaN and Inf: one FMA per value flags them (fminf/fmaxf skip NaNs)
-    float nz[4] = {0.f, 0.f, 0.f, 0.f};
+    // x * 0 is NaN exactly for NaN and Inf: one paired FMA per two values flags them (fminf/fmaxf skip NaNs)
+    float2 nz0 = make_float2(0.f, 0.f), nz1 = nz0;
+    const float2 zero2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
@@ -172,10 +187,11 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
         for (int c = 0; c < 4; ++c) {
             mn = fminf(mn, e[c]);
             mx = fmaxf(mx, e[c]);
-            nz[c] = __fmaf_rn(e[c], 0.f, nz[c]);
         }
+        nz0 = __ffma2_rn(make_float2(v[u].x, v[u].y), zero2, nz0);
+        nz1 = __ffma2_rn(make_float2(v[u].z, v[u].w), zero2, nz1);
     }
-    const float nzs = __fadd_rn(__fadd_rn(nz[0], nz[1]), __fadd_rn(nz[2], nz[3]));
+    const float nzs = __fadd_rn(__fadd_rn(nz0.x, nz0.y), __fadd_rn(nz1.x, nz1.y));
     const bool nan = nzs != nzs;
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 8));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
@@ -194,14 +210,19 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     // every clamp, so the min gives the same code.  When q <= 16 the pattern itself (2^23 + code) is
     // kept: the transpose below only uses its low 16 bits, which are the code's.  scale = 0 (a
     // (near-)constant block) makes every code 0
-    auto code = [&](float x) -> uint32_t {
-        const uint32_t bits = __float_as_uint(__fadd_rd(__fmul_rn(__fsub_rn(x, mn), scale), 0x1p23f));
-        return TWO ? min(cmax, bits - 0x4B000000u) : min(cmax + 0x4B000000u, bits);
+    // two values per paired-fp32 op: the same IEEE operations as fadd_rd(fmul(fsub(x, mn), scale), 2^23)
+    const float2 nmn = make_float2(-mn, -mn), sc2 = make_float2(scale, scale), big = make_float2(0x1p23f, 0x1p23f);
+    auto code2 = [&](float a, float b) -> uint2 {
+        const float2 t = fadd2_rd(__fmul2_rn(__fadd2_rn(make_float2(a, b), nmn), sc2), big);
+        const uint32_t ba = __float_as_uint(t.x), bb = __float_as_uint(t.y);
+        return TWO ? make_uint2(min(cmax, ba - 0x4B000000u), min(cmax, bb - 0x4B000000u))
+                   : make_uint2(min(cmax + 0x4B000000u, ba), min(cmax + 0x4B000000u, bb));
     };
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int r = r0 + 4 * u;  // r = yi + 4 zi, so j = xi + 4 r
-        *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) = make_uint4(code(v[u].x), code(v[u].y), code(v[u].z), code(v[u].w));
+        const uint2 c01 = code2(v[u].x, v[u].y), c23 = code2(v[u].z, v[u].w);
+        *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) = make_uint4(c01.x, c01.y, c23.x, c23.y);
     }
     __syncwarp();
     // ---- bit planes: lane m of the transpose owns plane (m & 15), half (m >> 4)
