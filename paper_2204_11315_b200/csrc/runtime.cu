@@ -98,8 +98,18 @@ static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 // helpers on the geometry
 // ---------------------------------------------------------------------------
 static inline uint64_t pb(const Plan *p) { return (uint64_t)p->geo.plane_bytes; }
-// byte offset of interior plane z inside one array of the host store
-static inline uint64_t hoff(const Plan *p, int64_t z) { return (uint64_t)(z - p->geo.store_lo) * pb(p); }
+// Bytes of one plane of one array in the store.  The uncompressed BASELINE keeps its pinned host store
+// in the working buffer's own pitched layout (rows of `pitch` floats, data at column XOFF), so that its
+// H2D / D2H / carry are 1-D copies straight between store and working set: a pitched 2-D H2D of
+// 4 KB rows was measured at 30.7 GB/s vs 55.5 GB/s for a 1-D copy (tools/memcpy2d_micro.py).  Every
+// other store holds the codec's planes (plane_bytes).
+static inline bool pitched_store(const Geometry &g) { return g.host_store && g.cfg.mode == OOCS_MODE_BASELINE; }
+static inline uint64_t store_pb(const Geometry &g) {
+    return pitched_store(g) ? (uint64_t)g.ay * g.pitch * 4 : (uint64_t)g.plane_bytes;
+}
+static inline uint64_t spb(const Plan *p) { return store_pb(p->geo); }
+// byte offset of interior plane z inside one array of the store
+static inline uint64_t hoff(const Plan *p, int64_t z) { return (uint64_t)(z - p->geo.store_lo) * spb(p); }
 // device store: same indexing
 static inline float *wsa(Plan *p, int set, int a) { return p->ws[set][a]; }
 
@@ -289,13 +299,13 @@ static Sizes compute_sizes(const Geometry &g) {
         z.staging = g.lanes * z.hfb;
         z.total += z.staging;
     }
-    z.arr_store = (size_t)g.store_planes() * g.plane_bytes;
+    z.arr_store = (size_t)g.store_planes() * store_pb(g);
     z.store_bytes = N_ARRAYS * z.arr_store;
     if (!g.host_store) z.total += al(z.arr_store) * 5;  // v + 2x(p_prev, p_curr)
     z.resident_vel = (g.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
     if (z.resident_vel) z.total += al(z.arr_store);
     if (g.cfg.world > 1) {
-        z.xbytes = (uint64_t)2 * g.k * R * g.plane_bytes;
+        z.xbytes = (uint64_t)2 * g.k * R * store_pb(g);
         z.total += 4 * al(z.xbytes);
     }
     z.total += 256;  // error flag
@@ -486,7 +496,7 @@ static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
     }
     for (int c = 0; c < 3; ++c) CU(cudaStreamSynchronize(p->cstream[c]));
     cudaStream_t st = p->lanes[0];
-    const uint64_t arr = (uint64_t)kR * pb(p);
+    const uint64_t arr = (uint64_t)kR * spb(p);
     // pack: planes [Zlo, Zlo+kR) -> send_lo ; [Zhi-kR, Zhi) -> send_hi ; arrays 1, 2
     for (int a = 1; a <= 2; ++a) {
         const uint64_t o = (uint64_t)(a - 1) * arr;
@@ -546,16 +556,16 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         break;
     case OOCS_OP_H2D: {
         const int64_t nplanes = b.body_hi - b.body_lo, off = b.body_lo - b.ext_lo;
-        if (g.cfg.mode == OOCS_MODE_BASELINE) {
+        if (g.cfg.mode == OOCS_MODE_BASELINE) {  // pitched store: one 1-D copy per array
             for (int a = 0; a < N_ARRAYS; ++a)
-                CU(copy_raw_to_ws(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), g, nplanes,
-                                  cudaMemcpyHostToDevice, st, p->copy_chunk));
+                CU(copy_1d(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), nplanes * spb(p),
+                           cudaMemcpyHostToDevice, st, p->copy_chunk));
         } else {
             for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
                 CU(copy_1d(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB, p->hstore[a] + hoff(p, b.body_lo),
                            nplanes * PB, cudaMemcpyHostToDevice, st, p->copy_chunk));
         }
-        if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
+        if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * spb(p);
         break;
     }
     case OOCS_OP_CARRY: {
@@ -567,9 +577,8 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
             // lane of o is the previous chunk's lane; destination is chunk g's working set
             const int wprev = (int)((o.g - 1) % g.n_ws);
             for (int a = 0; a < N_ARRAYS; ++a)
-                CU(cudaMemcpy2DAsync(wsa(p, w, a) + dst_off * g.pstride, g.pitch * 4,
-                                     wsa(p, wprev, a) + src_off * g.pstride, g.pitch * 4, g.pitch * 4,
-                                     nplanes * g.ay, cudaMemcpyDeviceToDevice, st));
+                CU(cudaMemcpyAsync(wsa(p, w, a) + dst_off * g.pstride, wsa(p, wprev, a) + src_off * g.pstride,
+                                   (size_t)nplanes * g.pstride * 4, cudaMemcpyDeviceToDevice, st));
             if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
         } else {
             const int sp = (int)((o.g - 1) % g.lanes);
@@ -639,16 +648,16 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         if (g.cfg.mode == OOCS_MODE_BASELINE) {
             const int curr = upd_array(g.k), prev = 3 - curr;
             const int64_t off = b.own_lo - b.ext_lo;
-            CU(copy_ws_to_raw(p->hstore[1] + hoff(p, b.own_lo), wsa(p, w, prev) + off * g.pstride, g, W,
-                              cudaMemcpyDeviceToHost, st, p->copy_chunk));
-            CU(copy_ws_to_raw(p->hstore[2] + hoff(p, b.own_lo), wsa(p, w, curr) + off * g.pstride, g, W,
-                              cudaMemcpyDeviceToHost, st, p->copy_chunk));
+            CU(copy_1d(p->hstore[1] + hoff(p, b.own_lo), wsa(p, w, prev) + off * g.pstride, W * spb(p),
+                       cudaMemcpyDeviceToHost, st, p->copy_chunk));
+            CU(copy_1d(p->hstore[2] + hoff(p, b.own_lo), wsa(p, w, curr) + off * g.pstride, W * spb(p),
+                       cudaMemcpyDeviceToHost, st, p->copy_chunk));
         } else {
             for (int j = 0; j < 2; ++j)
                 CU(copy_1d(p->hstore[1 + j] + hoff(p, b.own_lo), p->hf[s] + (uint64_t)j * g.max_own * PB, W * PB,
                            cudaMemcpyDeviceToHost, st, p->copy_chunk));
         }
-        if (stats) stats->bytes_d2h += (uint64_t)2 * W * PB;
+        if (stats) stats->bytes_d2h += (uint64_t)2 * W * spb(p);
         break;
     }
     case OOCS_OP_EXCHANGE: {
@@ -1013,7 +1022,9 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
         const int64_t n = std::min(chunk, a_hi - a);
         CU(copy_raw_to_ws(ws, src + (a - a_lo) * g.ax * g.ay, g, n, cudaMemcpyHostToDevice, s));
         const int64_t z = a - R;
-        if (g.host_store) {
+        if (pitched_store(g)) {  // BASELINE: the store holds working-buffer rows
+            CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), ws, n * spb(p), cudaMemcpyDeviceToHost, s));
+        } else if (g.host_store) {
             oocs_status r = k_encode(p, ws, stage, n, s, nullptr);
             if (r) return r;
             CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), stage, n * pb(p), cudaMemcpyDeviceToHost, s));
@@ -1049,14 +1060,18 @@ static oocs_status store(Plan *p, int32_t array, float *dst, int64_t a_lo, int64
         const int64_t n = std::min(chunk, a_hi - a);
         const int64_t z = a - R;
         const void *src;
-        if (g.host_store) {
-            CU(cudaMemcpyAsync(stage, p->hstore[array] + hoff(p, z), n * pb(p), cudaMemcpyHostToDevice, s));
-            src = stage;
+        if (pitched_store(g)) {
+            CU(cudaMemcpyAsync(ws, p->hstore[array] + hoff(p, z), n * spb(p), cudaMemcpyHostToDevice, s));
         } else {
-            src = p->dstore[array == 0 ? 0 : p->cur][array] + hoff(p, z);
+            if (g.host_store) {
+                CU(cudaMemcpyAsync(stage, p->hstore[array] + hoff(p, z), n * pb(p), cudaMemcpyHostToDevice, s));
+                src = stage;
+            } else {
+                src = p->dstore[array == 0 ? 0 : p->cur][array] + hoff(p, z);
+            }
+            oocs_status r = k_decode(p, src, ws, n, s, nullptr);
+            if (r) return r;
         }
-        oocs_status r = k_decode(p, src, ws, n, s, nullptr);
-        if (r) return r;
         CU(copy_ws_to_raw(dst + (a - a_lo) * g.ax * g.ay, ws, g, n, cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
     }
@@ -1069,6 +1084,17 @@ static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int6
     const Geometry &g = p->geo;
     CU(cudaSetDevice(g.cfg.device));
     const uint64_t off = hoff(p, a_lo - R), n = (uint64_t)(a_hi - a_lo) * pb(p);
+    if (pitched_store(g)) {  // raw bytes are the identity codec's planes (rows of ax floats)
+        const int64_t rows = (a_hi - a_lo) * g.ay;
+        uint8_t *base = p->hstore[array] + off + XOFF * 4;
+        for (int64_t r = 0; r < rows; ++r) {
+            uint8_t *st_row = base + (uint64_t)r * g.pitch * 4;
+            uint8_t *h_row = static_cast<uint8_t *>(host) + (uint64_t)r * g.ax * 4;
+            if (write) std::memcpy(st_row, h_row, g.ax * 4);
+            else std::memcpy(h_row, st_row, g.ax * 4);
+        }
+        return OOCS_OK;
+    }
     if (g.host_store) {
         if (write) {
             std::memcpy(p->hstore[array] + off, host, n);
