@@ -325,29 +325,30 @@ __device__ __forceinline__ int64_t tr16_ws_off(int q, int ax4, int64_t pitch) {
     return row * pitch + 4 * (q - row * ax4);
 }
 
-__global__ void tr16_encode_kernel(const float *__restrict__ src, uint4 *__restrict__ dst, int plane8, int ax4,
-                                   int64_t pitch, int64_t pstride) {
-    const float *s = src + (int64_t)blockIdx.y * pstride + XOFF;
-    uint4 *d = dst + (int64_t)blockIdx.y * plane8;
-    const int stride = gridDim.x * blockDim.x;
-    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < plane8; i0 += 4 * stride) {
+// The ws side is addressed by global row: rows of all planes are contiguous at `pitch` floats
+// (pstride = ay * pitch), so a flat 4-group index q maps to row q / ax4, column 4 (q mod ax4).
+__global__ void tr16_encode_kernel(const float *__restrict__ src, uint4 *__restrict__ dst, uint32_t n8, int ax4,
+                                   int64_t pitch) {
+    const float *s = src + XOFF;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n8; i0 += 4 * stride) {
         float4 v[4][2];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int i = i0 + j * stride;
-            if (i < plane8) {
+            const uint32_t i = i0 + j * stride;
+            if (i < n8) {
                 v[j][0] = __ldcs(reinterpret_cast<const float4 *>(s + tr16_ws_off(2 * i, ax4, pitch)));
                 v[j][1] = __ldcs(reinterpret_cast<const float4 *>(s + tr16_ws_off(2 * i + 1, ax4, pitch)));
             }
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int i = i0 + j * stride;
-            if (i < plane8)
-                __stcs(d + i, make_uint4(tr16_bits(v[j][0].x) | tr16_bits(v[j][0].y) << 16,
-                                         tr16_bits(v[j][0].z) | tr16_bits(v[j][0].w) << 16,
-                                         tr16_bits(v[j][1].x) | tr16_bits(v[j][1].y) << 16,
-                                         tr16_bits(v[j][1].z) | tr16_bits(v[j][1].w) << 16));
+            const uint32_t i = i0 + j * stride;
+            if (i < n8)
+                __stcs(dst + i, make_uint4(tr16_bits(v[j][0].x) | tr16_bits(v[j][0].y) << 16,
+                                           tr16_bits(v[j][0].z) | tr16_bits(v[j][0].w) << 16,
+                                           tr16_bits(v[j][1].x) | tr16_bits(v[j][1].y) << 16,
+                                           tr16_bits(v[j][1].z) | tr16_bits(v[j][1].w) << 16));
         }
     }
 }
@@ -357,31 +358,47 @@ __device__ __forceinline__ float4 tr16_expand(uint32_t lo, uint32_t hi) {
                        __uint_as_float(hi & 0xFFFF0000u));
 }
 
-__global__ void tr16_decode_kernel(const uint4 *__restrict__ src, float *__restrict__ dst, int plane8, int ax4,
-                                   int64_t pitch, int64_t pstride) {
-    const uint4 *s = src + (int64_t)blockIdx.y * plane8;
-    float *d = dst + (int64_t)blockIdx.y * pstride + XOFF;
-    const int stride = gridDim.x * blockDim.x;
-    for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < plane8; i0 += 4 * stride) {
-        uint4 u[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (i0 + j * stride < plane8) u[j] = __ldcs(s + i0 + j * stride);
+__global__ void tr16_decode_kernel(const uint2 *__restrict__ src, float *__restrict__ dst, uint32_t rows, int ax4,
+                                   int64_t pitch) {
+    // one 4-group (8 B in, 16 B out) per thread and step, consecutive lanes on consecutive bytes; every
+    // row is widened by one zero group on each side (pad columns XOFF-4.. and ax.., never read), so a
+    // row's stores span whole 32-byte sectors (XOFF-4 = 24 floats = 96 B); 4 steps in flight per thread
+    const int w = ax4 + 2;
+    const uint32_t n = rows * (uint32_t)w;
+    float *d = dst + XOFF - 4;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        uint2 u[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int i = i0 + j * stride;
-            if (i < plane8) {
-                __stcs(reinterpret_cast<float4 *>(d + tr16_ws_off(2 * i, ax4, pitch)), tr16_expand(u[j].x, u[j].y));
-                __stcs(reinterpret_cast<float4 *>(d + tr16_ws_off(2 * i + 1, ax4, pitch)), tr16_expand(u[j].z, u[j].w));
-            }
+            const uint32_t i = i0 + j * stride;
+            const uint32_t row = i / w;
+            const int c = (int)(i - row * w) - 1;
+            u[j] = make_uint2(0u, 0u);
+            if (i < n && c >= 0 && c < ax4) u[j] = __ldcs(src + (uint64_t)row * ax4 + c);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t i = i0 + j * stride;
+            const uint32_t row = i / w;
+            if (i < n)
+                __stcs(reinterpret_cast<float4 *>(d + row * pitch + 4 * (i - row * w)), tr16_expand(u[j].x, u[j].y));
         }
     }
 }
 
-static dim3 tr16_grid(int64_t plane8, int64_t planes) {
-    // about 8 resident 256-thread CTAs per SM over all planes, each thread doing >= 4 words per pass
-    const int64_t want = std::max<int64_t>(1, 148 * 8 / std::max<int64_t>(planes, 1));
-    return dim3((unsigned)std::min<int64_t>((plane8 + 1023) / 1024, want), (unsigned)planes);
+// one wave of resident CTAs over the whole range (a 2-D per-plane grid left 1.33 waves: ncu)
+template <typename K>
+static unsigned tr16_grid(K kernel, uint64_t n8) {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 148, per = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, 0);
+        blocks = sms * std::max(per, 1);
+    }
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)blocks, (n8 + 1023) / 1024));
 }
 
 // ---------------------------------------------------------------------------
@@ -1039,12 +1056,13 @@ cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, i
         return cudaGetLastError();
     }
     if (codec == 3) {
-        const int64_t plane8 = ay * ax / 8;  // ax, ay multiples of 4
-        for (int64_t z = 0; z < planes; z += 65535) {  // gridDim.y <= 65535
-            const int64_t n = std::min<int64_t>(planes - z, 65535);
-            tr16_decode_kernel<<<tr16_grid(plane8, n), 256, 0, st>>>(static_cast<const uint4 *>(src) + z * plane8,
-                                                                    dst + z * pstride, (int)plane8, (int)(ax / 4),
-                                                                    pitch, pstride);
+        // flat over all planes in launches of < 2^31 words (32-bit indices); ax, ay multiples of 4
+        const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
+        for (int64_t z = 0; z < planes; z += per) {
+            const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
+            tr16_decode_kernel<<<tr16_grid(tr16_decode_kernel, n8), 256, 0, st>>>(
+                static_cast<const uint2 *>(src) + 2 * z * plane8, dst + z * pstride,
+                (uint32_t)(std::min(per, planes - z) * ay), (int)(ax / 4), pitch);
         }
         return cudaGetLastError();
     }
@@ -1085,12 +1103,11 @@ cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, i
         return cudaGetLastError();
     }
     if (codec == 3) {
-        const int64_t plane8 = ay * ax / 8;
-        for (int64_t z = 0; z < planes; z += 65535) {
-            const int64_t n = std::min<int64_t>(planes - z, 65535);
-            tr16_encode_kernel<<<tr16_grid(plane8, n), 256, 0, st>>>(src + z * pstride,
-                                                                    static_cast<uint4 *>(dst) + z * plane8,
-                                                                    (int)plane8, (int)(ax / 4), pitch, pstride);
+        const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
+        for (int64_t z = 0; z < planes; z += per) {
+            const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
+            tr16_encode_kernel<<<tr16_grid(tr16_encode_kernel, n8), 256, 0, st>>>(
+                src + z * pstride, static_cast<uint4 *>(dst) + z * plane8, (uint32_t)n8, (int)(ax / 4), pitch);
         }
         return cudaGetLastError();
     }
