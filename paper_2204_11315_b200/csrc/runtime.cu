@@ -444,7 +444,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
     {
         // piece size of the pipeline's PCIe copies (OOCS_COPY_CHUNK_MB overrides; 0 = whole copies)
         const char *env = std::getenv("OOCS_COPY_CHUNK_MB");
-        p->copy_chunk = (env ? (uint64_t)std::strtoull(env, nullptr, 10) : 0ull) << 20;
+        p->copy_chunk = env ? (uint64_t)(std::strtod(env, nullptr) * 1048576.0) & ~uint64_t(15) : 0;
     }
     for (int l = 0; l < g.lanes; ++l) {
         if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||

@@ -49,3 +49,25 @@ def test_bad_arenas_are_rejected():
         with pytest.raises(oocs.OocsError) as e:
             oocs.oocs_plan_create_in(cfg, ptr, nbytes)
         assert e.value.status == 2
+
+
+@pytest.mark.parametrize("mode", ["swb", "baseline"])
+def test_chunked_pcie_copies_are_bitwise_equal(mode, monkeypatch):
+    """OOCS_COPY_CHUNK_MB splits every pipeline H2D/D2H into pieces (an experiment knob): the
+    same bytes must arrive, for the codec pipeline and the pitched-store BASELINE."""
+    nx, ny, nz, n, k = 40, 32, 64, 4, 2
+    vel, p0 = synth.fields(nx, ny, nz)
+    az = vel.shape[0]
+    codec = "identity" if mode == "baseline" else "blockquant"
+    cfg = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, rate_bits=16,
+                           codec=codec, mode=mode, store="host")
+    outs = []
+    for chunk in ("0", "0.004"):  # whole copies; 4 KB pieces
+        monkeypatch.setenv("OOCS_COPY_CHUNK_MB", chunk)
+        pl = oocs.Plan(cfg)
+        for a, arr in enumerate((vel, p0, p0)):
+            pl.load(a, arr, 0, az)
+        pl.run(3 * k)
+        outs.append([pl.read_raw(a, 0, az) for a in (1, 2)])
+        pl.close()
+    assert all(np.array_equal(x, y) for x, y in zip(*outs))
