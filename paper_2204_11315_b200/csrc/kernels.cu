@@ -79,11 +79,11 @@ __device__ __forceinline__ float2 fadd2_rd(float2 a, float2 b) {
 struct LineTask {
     int bz, by, b0, nb;
 };
-__device__ __forceinline__ LineTask line_task(int nbx) {
+__device__ __forceinline__ LineTask line_task(int nbx, int bz) {
     LineTask t;
     const int L = blockIdx.x;
     t.by = blockIdx.y * 8 + (threadIdx.x >> 5);
-    t.bz = blockIdx.z;
+    t.bz = bz;
     t.b0 = L == 0 ? 0 : 8 * L - 7;
     const int b1 = min(nbx - 1, 8 * L);
     t.nb = b1 - t.b0 + 1;
@@ -91,6 +91,17 @@ __device__ __forceinline__ LineTask line_task(int nbx) {
 }
 
 constexpr int CODEC_WARPS = 8;
+
+// up to 3 arrays of one chunk in one launch (grid z = array * slabs + slab): one ramp and one tail
+// per chunk instead of one per array
+struct CodecArrays {
+    const void *src[N_ARRAYS];
+    void *dst[N_ARRAYS];
+    int slabs;  // 4-plane slabs per array
+    // selects, not a dynamic index: an indexed kernel-parameter array would be copied to local memory
+    __device__ __forceinline__ const void *in(int a) const { return a == 0 ? src[0] : a == 1 ? src[1] : src[2]; }
+    __device__ __forceinline__ void *out(int a) const { return a == 0 ? dst[0] : a == 1 ? dst[1] : dst[2]; }
+};
 constexpr int CODE_LD = 68;  // padded per-block code row (u32)
 
 // ---------------------------------------------------------------------------
@@ -100,12 +111,14 @@ constexpr int CODE_LD = 68;  // padded per-block code row (u32)
 // ---------------------------------------------------------------------------
 template <bool TWO, int QT>
 __global__ void __launch_bounds__(CODEC_WARPS * 32)
-bq_decode_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int nbx, int nby,
-                 int64_t pitch, int64_t pstride, int q_rt) {
+bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t pstride, int q_rt) {
     const int q = QT ? QT : q_rt;
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const LineTask t = line_task(nbx);
+    const int arr = blockIdx.z / A.slabs;
+    const uint8_t *__restrict__ src = static_cast<const uint8_t *>(A.in(arr));
+    float *__restrict__ dst = static_cast<float *>(A.out(arr));
+    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
     if (t.by >= nby) return;
     const int recw = 2 * (q + 1);  // record size in 32-bit words
     const uint32_t *rec0 = reinterpret_cast<const uint32_t *>(src) +
@@ -255,12 +268,15 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
 // every time level, so any array of the working set is a valid source.
 template <bool TWO, int QT>
 __global__ void __launch_bounds__(CODEC_WARPS * 32)
-bq_encode_kernel(const float *__restrict__ src, uint8_t *__restrict__ dst, int nbx, int nby,
-                 int64_t pitch, int64_t pstride, int q_rt, int *err, int edge) {
+bq_encode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t pstride, int q_rt, int *err,
+                 int edge) {
     const int q = QT ? QT : q_rt;
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    LineTask t = line_task(nbx);
+    const int arr = blockIdx.z / A.slabs;
+    const float *__restrict__ src = static_cast<const float *>(A.in(arr));
+    uint8_t *__restrict__ dst = static_cast<uint8_t *>(A.out(arr));
+    LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
     if (edge == 1) {
         t.b0 = blockIdx.x ? nbx - 1 : 0;
         t.nb = 1;
@@ -1045,95 +1061,110 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
 // ---------------------------------------------------------------------------
 static inline int64_t nlines_of(int64_t ax) { return (XOFF + ax + 31) / 32; }
 
-cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
-                          int codec, int q, cudaStream_t st) {
-    if (planes <= 0) return cudaSuccess;
+cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, int64_t ax, int64_t ay,
+                          int64_t planes, int64_t pitch, int codec, int q, cudaStream_t st) {
+    if (planes <= 0 || n_arr <= 0) return cudaSuccess;
+    if (n_arr > N_ARRAYS) return cudaErrorInvalidValue;
     const int64_t pstride = ay * pitch;
-    if (codec == 2) {  // ZFP: q carries the rate
+    if (codec == 1) {  // BlockQuant: all arrays in one launch
         const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-        const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
-        zfp_decode_kernel<<<grid, 128, 0, st>>>(static_cast<const uint64_t *>(src), dst, nbx, nby, pitch, pstride, q);
-        return cudaGetLastError();
-    }
-    if (codec == 3) {
-        // flat over all planes in launches of < 2^31 words (32-bit indices); ax, ay multiples of 4
-        const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
-        for (int64_t z = 0; z < planes; z += per) {
-            const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
-            tr16_decode_kernel<<<tr16_grid(tr16_decode_kernel, n8), 256, 0, st>>>(
-                static_cast<const uint2 *>(src) + 2 * z * plane8, dst + z * pstride,
-                (uint32_t)(std::min(per, planes - z) * ay), (int)(ax / 4), pitch);
+        const int nl = (int)nlines_of(ax);
+        CodecArrays A{};
+        for (int a = 0; a < n_arr; ++a) {
+            A.src[a] = src[a];
+            A.dst[a] = dst[a];
         }
-        return cudaGetLastError();
-    }
-    if (codec == 0) {
-        const int64_t n4 = planes * ay * (ax / 4);
-        const int threads = 256;
-        const int64_t blocks = std::min<int64_t>((n4 + threads - 1) / threads, 148 * 16);
-        id_decode_kernel<<<(unsigned)blocks, threads, 0, st>>>(static_cast<const float4 *>(src), dst, n4,
-                                                              (int)(ax / 4), pitch);
-        return cudaGetLastError();
-    }
-    const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-    const int nl = (int)nlines_of(ax);
-    const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(planes / 4));
-    const uint8_t *s8 = static_cast<const uint8_t *>(src);
-#define DEC(TWO, QT) bq_decode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(s8, dst, nbx, nby, pitch, pstride, q)
-    switch (q) {  // the BASELINE.json rate sweep 8/12/16/24 bits/value gets constant-folded kernels
-    case 7: DEC(false, 7); break;
-    case 11: DEC(false, 11); break;
-    case 15: DEC(false, 15); break;
-    case 23: DEC(true, 23); break;
-    default:
-        if (q > 16) DEC(true, 0);
-        else DEC(false, 0);
-    }
+        A.slabs = (int)(planes / 4);
+        const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(A.slabs * n_arr));
+#define DEC(TWO, QT) bq_decode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q)
+        switch (q) {  // the BASELINE.json rate sweep 8/12/16/24 bits/value gets constant-folded kernels
+        case 7: DEC(false, 7); break;
+        case 11: DEC(false, 11); break;
+        case 15: DEC(false, 15); break;
+        case 23: DEC(true, 23); break;
+        default:
+            if (q > 16) DEC(true, 0);
+            else DEC(false, 0);
+        }
 #undef DEC
+        return cudaGetLastError();
+    }
+    for (int a = 0; a < n_arr; ++a) {
+        if (codec == 2) {  // ZFP: q carries the rate
+            const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+            const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
+            zfp_decode_kernel<<<grid, 128, 0, st>>>(static_cast<const uint64_t *>(src[a]), dst[a], nbx, nby, pitch,
+                                                    pstride, q);
+        } else if (codec == 3) {
+            // flat over all planes in launches of < 2^31 words (32-bit indices); ax, ay multiples of 4
+            const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
+            for (int64_t z = 0; z < planes; z += per) {
+                const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
+                tr16_decode_kernel<<<tr16_grid(tr16_decode_kernel, n8), 256, 0, st>>>(
+                    static_cast<const uint2 *>(src[a]) + 2 * z * plane8, dst[a] + z * pstride,
+                    (uint32_t)(std::min(per, planes - z) * ay), (int)(ax / 4), pitch);
+            }
+        } else {
+            const int64_t n4 = planes * ay * (ax / 4);
+            const int threads = 256;
+            const int64_t blocks = std::min<int64_t>((n4 + threads - 1) / threads, 148 * 16);
+            id_decode_kernel<<<(unsigned)blocks, threads, 0, st>>>(static_cast<const float4 *>(src[a]), dst[a], n4,
+                                                                  (int)(ax / 4), pitch);
+        }
+    }
     return cudaGetLastError();
 }
 
-cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
-                          int codec, int q, int *err, cudaStream_t st) {
-    if (planes <= 0) return cudaSuccess;
+cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, int64_t ax, int64_t ay,
+                          int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st) {
+    if (planes <= 0 || n_arr <= 0) return cudaSuccess;
+    if (n_arr > N_ARRAYS) return cudaErrorInvalidValue;
     const int64_t pstride = ay * pitch;
-    if (codec == 2) {  // ZFP: q carries the rate
+    if (codec == 1) {  // BlockQuant: all arrays in one launch
         const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-        const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
-        zfp_encode_kernel<<<grid, 128, 0, st>>>(src, static_cast<uint64_t *>(dst), nbx, nby, pitch, pstride, q, err);
-        return cudaGetLastError();
-    }
-    if (codec == 3) {
-        const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
-        for (int64_t z = 0; z < planes; z += per) {
-            const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
-            tr16_encode_kernel<<<tr16_grid(tr16_encode_kernel, n8), 256, 0, st>>>(
-                src + z * pstride, static_cast<uint4 *>(dst) + z * plane8, (uint32_t)n8, (int)(ax / 4), pitch);
+        const int nl = (int)nlines_of(ax);
+        CodecArrays A{};
+        for (int a = 0; a < n_arr; ++a) {
+            A.src[a] = src[a];
+            A.dst[a] = dst[a];
         }
-        return cudaGetLastError();
-    }
-    if (codec == 0) {
-        const int64_t n4 = planes * ay * (ax / 4);
-        const int threads = 256;
-        const int64_t blocks = std::min<int64_t>((n4 + threads - 1) / threads, 148 * 16);
-        id_encode_kernel<<<(unsigned)blocks, threads, 0, st>>>(src, static_cast<float4 *>(dst), n4,
-                                                              (int)(ax / 4), pitch);
-        return cudaGetLastError();
-    }
-    const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-    const int nl = (int)nlines_of(ax);
-    const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(planes / 4));
-    uint8_t *d8 = static_cast<uint8_t *>(dst);
-#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 0)
-    switch (q) {
-    case 7: ENC(false, 7); break;
-    case 11: ENC(false, 11); break;
-    case 15: ENC(false, 15); break;
-    case 23: ENC(true, 23); break;
-    default:
-        if (q > 16) ENC(true, 0);
-        else ENC(false, 0);
-    }
+        A.slabs = (int)(planes / 4);
+        const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(A.slabs * n_arr));
+#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 0)
+        switch (q) {
+        case 7: ENC(false, 7); break;
+        case 11: ENC(false, 11); break;
+        case 15: ENC(false, 15); break;
+        case 23: ENC(true, 23); break;
+        default:
+            if (q > 16) ENC(true, 0);
+            else ENC(false, 0);
+        }
 #undef ENC
+        return cudaGetLastError();
+    }
+    for (int a = 0; a < n_arr; ++a) {
+        if (codec == 2) {  // ZFP: q carries the rate
+            const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+            const dim3 grid((unsigned)(((int64_t)nbx * nby + 127) / 128), (unsigned)(planes / 4));
+            zfp_encode_kernel<<<grid, 128, 0, st>>>(src[a], static_cast<uint64_t *>(dst[a]), nbx, nby, pitch,
+                                                    pstride, q, err);
+        } else if (codec == 3) {
+            const int64_t plane8 = ay * ax / 8, per = std::max<int64_t>(1, ((int64_t)1 << 30) / plane8);
+            for (int64_t z = 0; z < planes; z += per) {
+                const uint64_t n8 = (uint64_t)std::min(per, planes - z) * plane8;
+                tr16_encode_kernel<<<tr16_grid(tr16_encode_kernel, n8), 256, 0, st>>>(
+                    src[a] + z * pstride, static_cast<uint4 *>(dst[a]) + z * plane8, (uint32_t)n8, (int)(ax / 4),
+                    pitch);
+            }
+        } else {
+            const int64_t n4 = planes * ay * (ax / 4);
+            const int threads = 256;
+            const int64_t blocks = std::min<int64_t>((n4 + threads - 1) / threads, 148 * 16);
+            id_encode_kernel<<<(unsigned)blocks, threads, 0, st>>>(src[a], static_cast<float4 *>(dst[a]), n4,
+                                                                  (int)(ax / 4), pitch);
+        }
+    }
     return cudaGetLastError();
 }
 
@@ -1244,19 +1275,22 @@ cudaError_t launch_step_encode(const float *vel, const float *pprev, const float
     const int64_t pstride = ay * pitch;
     const int slabs = (int)((z_hi - z_lo) / 4);
     const float *src = pcurr + z_lo * pstride;
-    for (int j = 0; j < 2; ++j) {
-        uint8_t *d8 = static_cast<uint8_t *>(j ? out_curr : out_prev);
-        const dim3 gx2(2, (unsigned)((nby + 7) / 8), (unsigned)slabs), gy2((unsigned)nl, 1, (unsigned)slabs);
+    // both arrays in each launch (same source: the halo values are level-independent)
+    CodecArrays A{};
+    A.src[0] = A.src[1] = src;
+    A.dst[0] = out_prev;
+    A.dst[1] = out_curr;
+    A.slabs = slabs;
+    const dim3 gx2(2, (unsigned)((nby + 7) / 8), (unsigned)(2 * slabs)), gy2((unsigned)nl, 1, (unsigned)(2 * slabs));
 #define EDGE(TWO, QT)                                                                                        \
     do {                                                                                                     \
-        bq_encode_kernel<TWO, QT><<<gx2, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 1); \
-        bq_encode_kernel<TWO, QT><<<gy2, CODEC_WARPS * 32, 0, st>>>(src, d8, nbx, nby, pitch, pstride, q, err, 2); \
+        bq_encode_kernel<TWO, QT><<<gx2, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 1); \
+        bq_encode_kernel<TWO, QT><<<gy2, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 2); \
     } while (0)
-        if (q == 15) EDGE(false, 15);
-        else if (q > 16) EDGE(true, 0);
-        else EDGE(false, 0);
+    if (q == 15) EDGE(false, 15);
+    else if (q > 16) EDGE(true, 0);
+    else EDGE(false, 0);
 #undef EDGE
-    }
     return cudaGetLastError();
 }
 

@@ -39,10 +39,11 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *geo, std::string *er
 void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops);
 
 // kernels.cu
-cudaError_t launch_decode(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
-                          int codec, int q, cudaStream_t st);
-cudaError_t launch_encode(const float *src, void *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch,
-                          int codec, int q, int *err, cudaStream_t st);
+// n_arr (<= N_ARRAYS) arrays of the same geometry; BlockQuant does them in one launch
+cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, int64_t ax, int64_t ay,
+                          int64_t planes, int64_t pitch, int codec, int q, cudaStream_t st);
+cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, int64_t ax, int64_t ay,
+                          int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
 // last step fused with the BlockQuant encode of the owned slabs [z_lo, z_hi) (device store)

@@ -174,32 +174,42 @@ static KernelTiming *timing_slot(Plan *p, int kind) {
     return t;
 }
 
-static oocs_status k_decode(Plan *p, const void *src, float *dst, int64_t planes, cudaStream_t st,
-                            oocs_stats *stats) {
+// n arrays of `planes` planes each, one launch for BlockQuant (stats count launches as issued)
+static oocs_status k_decode(Plan *p, const void *const *src, float *const *dst, int n, int64_t planes,
+                            cudaStream_t st, oocs_stats *stats) {
     KernelTiming *t = timing_slot(p, 0);
     if (t) CU(cudaEventRecord(t->a, st));
-    CU(launch_decode(src, dst, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, st));
+    CU(launch_decode(src, dst, n, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, st));
     if (t) CU(cudaEventRecord(t->b, st));
     if (stats) {
-        stats->kernel_launches[0]++;
+        stats->kernel_launches[0] += p->geo.codec == OOCS_CODEC_BLOCKQUANT ? 1 : n;
         const uint64_t vals = (uint64_t)planes * p->geo.ax * p->geo.ay;
-        stats->alg_bytes[0] += (uint64_t)planes * pb(p) + vals * 4;
+        stats->alg_bytes[0] += n * ((uint64_t)planes * pb(p) + vals * 4);
     }
     return OOCS_OK;
 }
-
-static oocs_status k_encode(Plan *p, const float *src, void *dst, int64_t planes, cudaStream_t st,
+static oocs_status k_decode(Plan *p, const void *src, float *dst, int64_t planes, cudaStream_t st,
                             oocs_stats *stats) {
+    return k_decode(p, &src, &dst, 1, planes, st, stats);
+}
+
+static oocs_status k_encode(Plan *p, const float *const *src, void *const *dst, int n, int64_t planes,
+                            cudaStream_t st, oocs_stats *stats) {
     KernelTiming *t = timing_slot(p, 2);
     if (t) CU(cudaEventRecord(t->a, st));
-    CU(launch_encode(src, dst, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, p->d_err, st));
+    CU(launch_encode(src, dst, n, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.codec, p->geo.q, p->d_err,
+                     st));
     if (t) CU(cudaEventRecord(t->b, st));
     if (stats) {
-        stats->kernel_launches[2]++;
+        stats->kernel_launches[2] += p->geo.codec == OOCS_CODEC_BLOCKQUANT ? 1 : n;
         const uint64_t vals = (uint64_t)planes * p->geo.ax * p->geo.ay;
-        stats->alg_bytes[2] += vals * 4 + (uint64_t)planes * pb(p);
+        stats->alg_bytes[2] += n * (vals * 4 + (uint64_t)planes * pb(p));
     }
     return OOCS_OK;
+}
+static oocs_status k_encode(Plan *p, const float *src, void *dst, int64_t planes, cudaStream_t st,
+                            oocs_stats *stats) {
+    return k_encode(p, &src, &dst, 1, planes, st, stats);
 }
 
 static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, int64_t zlo, int64_t zhi,
@@ -591,17 +601,19 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         break;
     }
     case OOCS_OP_DECODE: {
+        const void *src[N_ARRAYS];
+        float *dst[N_ARRAYS];
         for (int a = 0; a < N_ARRAYS; ++a) {
-            const uint8_t *src;
             if (a == 0 && p->resident_vel)
-                src = p->dvel + hoff(p, b.ext_lo);
+                src[a] = p->dvel + hoff(p, b.ext_lo);
             else if (g.host_store)
-                src = p->hf[s] + (uint64_t)a * g.max_ext * PB;
+                src[a] = p->hf[s] + (uint64_t)a * g.max_ext * PB;
             else
-                src = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
-            oocs_status r = k_decode(p, src, wsa(p, w, a), E, st, stats);
-            if (r) return r;
+                src[a] = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
+            dst[a] = wsa(p, w, a);
         }
+        oocs_status r = k_decode(p, src, dst, N_ARRAYS, E, st, stats);
+        if (r) return r;
         break;
     }
     case OOCS_OP_STEP: {
@@ -632,15 +644,17 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         const int curr = upd_array(g.k), prev = 3 - curr;
         const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;
         const int src_arr[2] = {prev, curr};
+        const float *src[2];
+        void *dst[2];
         for (int j = 0; j < 2; ++j) {
-            void *dst;
+            src[j] = wsa(p, w, src_arr[j]) + off * g.pstride;
             if (g.host_store)
-                dst = p->hf[s] + (uint64_t)j * g.max_own * PB;
+                dst[j] = p->hf[s] + (uint64_t)j * g.max_own * PB;
             else
-                dst = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
-            oocs_status r = k_encode(p, wsa(p, w, src_arr[j]) + off * g.pstride, dst, W, st, stats);
-            if (r) return r;
+                dst[j] = p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo);
         }
+        oocs_status r = k_encode(p, src, dst, 2, W, st, stats);
+        if (r) return r;
         break;
     }
     case OOCS_OP_D2H: {
@@ -1237,7 +1251,7 @@ oocs_status oocs_decode(const void *src, float *dst, int64_t ax, int64_t ay, int
         return OOCS_ERR_CONFIG;
     }
     const int qk = codec == 1 ? rate_bits - 1 : codec == 2 ? rate_bits : 0;
-    CU(launch_decode(src, dst, ax, ay, planes, pitch, codec, qk, (cudaStream_t)stream));
+    CU(launch_decode(&src, &dst, 1, ax, ay, planes, pitch, codec, qk, (cudaStream_t)stream));
     return OOCS_OK;
 }
 
@@ -1265,7 +1279,7 @@ oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int
         if (!scratch[dev]) CU(cudaMalloc((void **)&scratch[dev], sizeof(int)));
         flag = scratch[dev];
     }
-    CU(launch_encode(src, dst, ax, ay, planes, pitch, codec, qk, flag, (cudaStream_t)stream));
+    CU(launch_encode(&src, &dst, 1, ax, ay, planes, pitch, codec, qk, flag, (cudaStream_t)stream));
     return OOCS_OK;
 }
 
