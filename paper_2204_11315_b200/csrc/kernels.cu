@@ -807,6 +807,12 @@ __device__ __forceinline__ void transpose32_regs(uint32_t *a) {
 #pragma unroll
         for (int r = 0; r < 32; ++r) {
             if (r & j) continue;
+            if (j >= 8) {  // whole bytes move: two byte permutes instead of the shift/xor swap
+                const uint32_t x = a[r], y = a[r | j];
+                a[r] = __byte_perm(x, y, j == 16 ? 0x5410 : 0x6240);
+                a[r | j] = __byte_perm(x, y, j == 16 ? 0x7632 : 0x7351);
+                continue;
+            }
             const uint32_t t = ((a[r] >> j) ^ a[r | j]) & m;
             a[r] ^= t << j;
             a[r | j] ^= t;
@@ -814,55 +820,69 @@ __device__ __forceinline__ void transpose32_regs(uint32_t *a) {
     }
 }
 
-struct BitWriter {
-    uint64_t *out;
+// LSB-first writer over 32-bit words: fewer than 32 bits pending in a 64-bit accumulator, so a put of
+// m <= 32 bits is a shift, an OR and a rarely divergent word store
+struct BitOut {
+    uint32_t *out;
     uint64_t cur;
-    int nb;  // bits pending in cur
-    __device__ __forceinline__ void put1(uint32_t b) {
-        cur |= (uint64_t)(b & 1u) << nb;
-        if (++nb == 64) {
-            *out++ = cur;
-            cur = 0;
-            nb = 0;
+    int nb;  // bits pending in cur (0..31)
+    __device__ __forceinline__ void put(uint32_t v, int m) {  // 0 <= m <= 32, v < 2^m
+        cur |= (uint64_t)v << nb;
+        nb += m;
+        if (nb >= 32) {
+            *out++ = (uint32_t)cur;
+            cur >>= 32;
+            nb -= 32;
         }
     }
-    __device__ __forceinline__ void put(uint64_t v, int m) {  // low m bits of v, 0 <= m <= 64
-        if (m == 0) return;
-        if (m < 64) v &= ((uint64_t)1 << m) - 1;
-        cur |= v << nb;
-        const int t = nb + m;
-        if (t >= 64) {
-            *out++ = cur;
-            cur = nb ? v >> (64 - nb) : 0;
-            nb = t - 64;
+    __device__ __forceinline__ void put64(uint64_t v, int m) {  // low m bits of v, 0 <= m <= 64
+        if (m <= 32) {
+            put(m == 32 ? (uint32_t)v : (uint32_t)v & ((1u << m) - 1u), m);
         } else {
-            nb = t;
+            put((uint32_t)v, 32);
+            const uint32_t hi = (uint32_t)(v >> 32);
+            put(m == 64 ? hi : hi & ((1u << (m - 32)) - 1u), m - 32);
         }
     }
 };
 
-// LSB-first reader with a two-word window: the next 64 bits are always one funnel shift away, so a
-// read of m <= 64 bits is a shift, a mask and an advance (bits past the record read as zeros)
-struct BitWin {
-    const uint64_t *in, *end;  // next word to load, end of the record
-    uint64_t lo, hi;           // current word, next word
-    int off;                   // bits of lo already consumed (0..63)
-    __device__ __forceinline__ void init(const uint64_t *p, int words) {
+// LSB-first reader over 32-bit words: a right-aligned 64-bit buffer that always holds >= 32 valid
+// bits, so the next 32 bits are one register read and consuming m <= 32 bits is a 64-bit shift plus a
+// rarely taken refill (bits past the record read as zeros)
+struct BitBuf {
+    const uint32_t *in, *end;  // next word to load, end of the record
+    uint64_t buf;
+    int cnt;       // valid bits in buf (32..64)
+    uint32_t nxt;  // the word after buf, loaded one refill ahead (its latency hides behind ~32 bits)
+    __device__ __forceinline__ void init(const uint32_t *p, int words) {
         end = p + words;
-        lo = __ldg(p);
-        hi = words > 1 ? __ldg(p + 1) : 0;
-        in = p + 2;
-        off = 0;
+        buf = (uint64_t)__ldg(p) | (words > 1 ? (uint64_t)__ldg(p + 1) << 32 : 0);
+        nxt = words > 2 ? __ldg(p + 2) : 0u;
+        in = p + 3;
+        cnt = 64;
     }
-    __device__ __forceinline__ uint64_t peek64() const { return off ? (lo >> off) | (hi << (64 - off)) : lo; }
-    __device__ __forceinline__ void skip(int m) {  // 0 <= m <= 64
-        off += m;
-        if (off >= 64) {
-            off -= 64;
-            lo = hi;
-            hi = in < end ? __ldg(in) : 0;
+    __device__ __forceinline__ uint32_t peek32() const { return (uint32_t)buf; }
+    __device__ __forceinline__ void consume(int m) {  // 0 <= m <= 32
+        buf >>= m;
+        cnt -= m;
+        if (cnt < 32) {
+            buf |= (uint64_t)nxt << cnt;
+            cnt += 32;
+            nxt = in < end ? __ldg(in) : 0u;
             ++in;
         }
+    }
+    __device__ __forceinline__ uint64_t read(int m) {  // 0 <= m <= 64
+        if (m <= 32) {
+            const uint32_t v = m == 32 ? peek32() : peek32() & ((1u << m) - 1u);
+            consume(m);
+            return v;
+        }
+        const uint32_t lo = peek32();
+        consume(32);
+        const uint32_t hi = m == 64 ? peek32() : peek32() & ((1u << (m - 32)) - 1u);
+        consume(m - 32);
+        return (uint64_t)lo | ((uint64_t)hi << 32);
     }
 };
 
@@ -878,8 +898,8 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (int64_t)nbx * nby) return;
     const int bx = (int)(t % nbx), by = (int)(t / nbx), bz = blockIdx.y;
-    const int words = rate;  // 64 * rate bits
-    uint64_t *rec = dst + ((int64_t)(bz * nby + by) * nbx + bx) * words;
+    const int words = 2 * rate;  // 64 * rate bits in 32-bit words
+    uint32_t *rec = reinterpret_cast<uint32_t *>(dst + ((int64_t)(bz * nby + by) * nbx + bx) * rate);
     float x[64];
     const float *s0 = src + (int64_t)(4 * bz) * pstride + (int64_t)(4 * by) * pitch + XOFF + 4 * bx;
 #pragma unroll
@@ -903,12 +923,12 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
         atomicOr(err, 1);
         return;
     }
-    BitWriter bw{rec, 0, 0};
+    BitOut bw{rec, 0, 0};
     if (amax > 0.f) {
         const int be = (int)(__float_as_uint(amax) >> 23);
         const int emax = max(be - 126, -126);  // frexp exponent, clamped for denormals
         const uint32_t e = (uint32_t)(emax + 127);
-        bw.put(2 * (uint64_t)e + 1, 9);
+        bw.put(2 * e + 1, 9);
         int32_t ib[64];
         if (emax >= -97) {  // 2^(30-emax) is a normal float: the float product is exact
             const float sc = __int_as_float((127 + 30 - emax) << 23);
@@ -938,7 +958,7 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
             uint64_t plane = zs_planes[k][threadIdx.x];
             const int m = min(n, bits);
             bits -= m;
-            bw.put(plane, m);
+            bw.put64(plane, m);
             plane = m == 64 ? 0 : plane >> m;
             // unary run-length code of the remainder, one step per newly significant coefficient:
             // group test bit, then the zeros up to the next 1 and that 1 (implied at position 63)
@@ -951,13 +971,16 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
                 const int z = __ffsll((long long)plane) - 1, zmax = 63 - n;
                 const int len = z < zmax ? z + 1 : zmax;  // bits the zfp loop would write
                 if (len <= bits) {  // group bit 1, z zeros and a 1 (implied when n reaches 63): one put
-                    bw.put(1u | (z < zmax ? (uint64_t)2 << z : 0), len + 1);
+                    if (len < 32)
+                        bw.put(1u | (z < zmax ? 2u << z : 0u), len + 1);
+                    else
+                        bw.put64(1u | (z < zmax ? (uint64_t)2 << z : 0), len + 1);
                     bits -= len;
                     const int adv = z < zmax ? z + 1 : zmax + 1;
                     n += adv;
                     plane = adv >= 64 ? 0 : plane >> adv;
                 } else {  // budget ends inside the zero run
-                    bw.put(1u, bits + 1);
+                    bw.put64(1u, bits + 1);
                     n += bits + 1;
                     plane = 0;
                     bits = 0;
@@ -965,10 +988,10 @@ zfp_encode_kernel(const float *__restrict__ src, uint64_t *__restrict__ dst, int
             }
         }
     } else {
-        bw.put1(0);
+        bw.put(0, 1);
     }
     // pad the record with zeros up to maxbits
-    if (bw.nb) *bw.out++ = bw.cur;
+    if (bw.nb) *bw.out++ = (uint32_t)bw.cur;
     while (bw.out < rec + words) *bw.out++ = 0;
 }
 
@@ -980,16 +1003,16 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
     if (t >= (int64_t)nbx * nby) return;
     const int bx = (int)(t % nbx), by = (int)(t / nbx), bz = blockIdx.y;
     const uint64_t *rec = src + ((int64_t)(bz * nby + by) * nbx + bx) * rate;
-    BitWin br;
-    br.init(rec, rate);
+    BitBuf br;
+    br.init(reinterpret_cast<const uint32_t *>(rec), 2 * rate);
     float x[64];
-    const uint64_t head = br.peek64();
+    const uint32_t head = br.peek32();
     if (!(head & 1u)) {
 #pragma unroll
         for (int j = 0; j < 64; ++j) x[j] = 0.f;
     } else {
         const int emax = (int)((head >> 1) & 0xFFu) - 127;
-        br.skip(9);
+        br.consume(9);
 #pragma unroll
         for (int k = 0; k < 32; ++k) zs_planes[k][threadIdx.x] = 0;
         int bits = 64 * rate - 9;
@@ -1000,23 +1023,49 @@ zfp_decode_kernel(const uint64_t *__restrict__ src, float *__restrict__ dst, int
             // the first n coefficients (already significant) are sent verbatim
             const int m = min(n, bits);
             bits -= m;
-            uint64_t plane = m == 0 ? 0 : m == 64 ? br.peek64() : br.peek64() & (((uint64_t)1 << m) - 1);
-            br.skip(m);
-            // then per newly significant coefficient: group-test bit 1, zeros, a 1 (implied at 63)
+            uint64_t plane = br.read(m);
+            // then per newly significant coefficient: group-test bit 1, zeros, a 1 (implied at 63); the
+            // inner zfp loop reads at most lim = min(63 - n, bits) run bits and leaves n at the 1 it
+            // found, or lim further on (budget or position 63 reached), where the bit is set either way
             while (n < 64 && bits > 0) {
                 bits--;
-                const uint64_t w = br.peek64();
+                const uint32_t w = br.peek32();
                 if (!(w & 1u)) {  // group test 0: nothing more in this plane
-                    br.skip(1);
+                    br.consume(1);
                     break;
                 }
-                const int avail = min(63 - n, bits);  // zeros the zfp loop may read before stopping
-                const uint64_t t = w >> 1;
-                const int z = min(t ? __ffsll((long long)t) - 1 : 64, avail);  // the next 1, or none in reach
-                const int used = z < avail ? z + 1 : avail;  // run of zeros (+ its terminating 1)
-                br.skip(1 + used);
-                bits -= used;
-                n += z;
+                const int lim = min(63 - n, bits);
+                const uint32_t t = w >> 1;  // the next 31 stream bits
+                if (t || lim <= 31) {
+                    const int z = min(t ? __ffs(t) - 1 : 31, lim);
+                    const int used = z < lim ? z + 1 : z;  // run of zeros (+ its terminating 1)
+                    br.consume(1 + used);
+                    bits -= used;
+                    n += z;
+                } else {  // >= 31 zeros and room for more: count the run word by word
+                    br.consume(1);
+                    int rem = lim;
+                    while (true) {
+                        const uint32_t w2 = br.peek32();
+                        const int zz = w2 ? __ffs(w2) - 1 : 32;
+                        if (zz < 32 && zz < rem) {  // the terminating 1
+                            br.consume(zz + 1);
+                            bits -= zz + 1;
+                            n += zz;
+                            break;
+                        }
+                        if (rem <= 32) {  // limit reached inside the run
+                            br.consume(rem);
+                            bits -= rem;
+                            n += rem;
+                            break;
+                        }
+                        br.consume(32);
+                        bits -= 32;
+                        n += 32;
+                        rem -= 32;
+                    }
+                }
                 plane |= (uint64_t)1 << n;
                 n++;
             }

@@ -45,7 +45,7 @@ def gpu_decode(buf, ax, ay, planes, rate):
     return from_ws(ws, ax)
 
 
-@pytest.mark.parametrize("rate", [1, 4, 8, 12, 16, 24, 32])
+@pytest.mark.parametrize("rate", [1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 31, 32])
 def test_zfp_bitstream_bit_exact(rate):
     planes, ay, ax = 8, 12, 44
     blocks = synth.random_blocks(planes * ay * ax // 64, seed=rate)
@@ -59,7 +59,32 @@ def test_zfp_bitstream_bit_exact(rate):
     vel, p0 = synth.fields(64, 64, 32)
     for a in (vel[:16], p0[12:28]):
         a = np.ascontiguousarray(a)
-        assert np.array_equal(gpu_encode(a, rate), oracle.encode_planes(a, ZFP, rate))
+        enc = oracle.encode_planes(a, ZFP, rate)
+        assert np.array_equal(gpu_encode(a, rate), enc)
+        # decode of smooth-field records (long zero runs, late significance) bitwise
+        pl, ay2, ax2 = a.shape
+        assert np.array_equal(gpu_decode(enc, ax2, ay2, pl, rate).view(np.uint32),
+                              oracle.decode_planes(enc, ax2, ay2, pl, ZFP, rate).view(np.uint32))
+
+
+@pytest.mark.parametrize("rate", [1, 2, 5, 16, 32])
+def test_zfp_decode_arbitrary_records(rate):
+    """The decoder's parser on arbitrary bit strings (every record is a valid fixed-rate stream): random
+    words, words with sparse ones (long zero runs across word boundaries, runs cut by the budget or by
+    position 63), all-ones -- bitwise equal to the oracle's decoder."""
+    planes, ay, ax = 4, 8, 32
+    nrec = (ay // 4) * (ax // 4) * (planes // 4)
+    rng = np.random.default_rng(rate)
+    words = rng.integers(0, 2**32, size=(nrec, 2 * rate), dtype=np.uint64).astype(np.uint32)
+    sparse = rng.random((nrec, 2 * rate, 32)) < 0.02
+    words[nrec // 3: 2 * nrec // 3] = (sparse[nrec // 3: 2 * nrec // 3] << np.arange(32)).sum(-1).astype(np.uint32)
+    words[-2:] = 0xFFFFFFFF
+    words[:, 0] |= 1  # non-zero blocks
+    words[:, 0] = (words[:, 0] & ~np.uint32(0x1FE)) | (np.uint32(127 + 3) << 1)  # emax = 3: finite values
+    buf = words.view(np.uint8).reshape(-1)
+    got = gpu_decode(buf, ax, ay, planes, rate)
+    want = oracle.decode_planes(buf, ax, ay, planes, ZFP, rate)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 @pytest.mark.parametrize("store,sched", [("host", "alg1"), ("device", "alg1"), ("host", "dag")])
