@@ -484,6 +484,18 @@ def main():
             reps += 1
         cpu = {"value": reps * cells / secs / 1e9, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
                "sample": f"{sample}, x{reps}", "seconds": secs}
+        # the same oracle on one core, on a quarter-width slab (all cores and 1 core)
+        import oracle
+
+        one1, cells1, sample1 = cpu_oracle_sample(nx // 4, ny // 4, k, rate, device=f"cuda:{local}",
+                                                  codec=args.codec)
+        oracle.set_threads(1)
+        try:
+            s1 = one1()
+        finally:
+            oracle.set_threads(threads_used())
+        cpu["one_core"] = {"value": cells1 / s1 / 1e9, "unit": UNIT, "cores": 1, "sample": sample1,
+                           "seconds": s1}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -91,6 +91,11 @@ class OracleError(RuntimeError):
         self.rc = rc
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's plane loops (timing only; results are thread-count independent)."""
+    lib().oracle_set_threads(int(n))
+
+
 def coeffs() -> np.ndarray:
     c = np.zeros(5, dtype=np.float64)
     lib().oracle_coeffs(_p(c))

@@ -52,6 +52,19 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Host threads for the OpenMP plane loops (timing only: results do not depend on it, every
+ * parallel loop writes disjoint planes). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
 
 #define R 4 /* stencil radius: 25-point star = centre + 3 axes x 2 sides x 4 (Table 1 HALO=4) */
 
