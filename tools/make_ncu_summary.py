@@ -1,0 +1,43 @@
+"""profiles/ncu_summary.json (bench.py's roofline.traffic source) from the three ncu --set full captures of
+tools/gpu_final.sh: DRAM bytes vs algorithmic bytes of the same launch, per kernel.
+
+usage: python tools/make_ncu_summary.py STEP.ncu-rep DECODE.ncu-rep ENCODE.ncu-rep STEP_PLANES
+Algorithmic bytes: stencil 16 B per cell-update (STEP_PLANES x 1024^2); codec (r/8 + 4) B per value,
+values = 4 * grid.z planes x 1032^2 (grid z = array x slab)."""
+import json
+import sys
+
+sys.path.insert(0, __import__("os").path.dirname(__file__))
+from ncu_summary import summarise  # noqa: E402
+
+RATE = 16
+AX = 1032
+
+
+def entry(rep, alg, unit):
+    e = summarise(rep)[0]
+    e["alg_bytes_per_launch"] = alg
+    e["alg_unit"] = unit
+    e["dram_bytes_per_launch"] = e["dram_bytes"]
+    e["traffic_over_alg"] = e["dram_bytes"] / alg
+    e["alg_gbs"] = alg / (e["duration_us"] * 1e-6) / 1e9
+    e["source"] = f"{rep} (ncu --set full --clock-control none, c2 workload, tools/profile_kernels.py)"
+    return {k: e[k] for k in ("kernel", "grid", "duration_us", "dram_bytes_per_launch", "alg_bytes_per_launch",
+                              "alg_unit", "traffic_over_alg", "dram_gbs", "alg_gbs", "issue_active_pct",
+                              "inst_executed", "registers", "top_stalls", "source") if k in e}
+
+
+def codec_values(rep):
+    gz = int(summarise(rep)[0]["grid"].strip("()").split(",")[2])
+    return 4 * gz * AX * AX, 4 * gz
+
+
+if __name__ == "__main__":
+    step, dec, enc, planes = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+    out = {"step": entry(step, planes * 1024 * 1024 * 16, f"{planes} planes x 1024^2 cell-updates x 16 B")}
+    for name, rep in (("decode", dec), ("encode", enc)):
+        v, pl = codec_values(rep)
+        out[name] = entry(rep, v * (RATE // 8 + 4), f"{pl} array-planes x {AX}^2 values x ({RATE // 8} + 4) B")
+    json.dump(out, open("profiles/ncu_summary.json", "w"), indent=1)
+    print(json.dumps({k: {x: v.get(x) for x in ("duration_us", "traffic_over_alg", "alg_gbs", "issue_active_pct")}
+                      for k, v in out.items()}, indent=1))

@@ -1,5 +1,5 @@
 """Representative launches for ncu: one c2 plan with the compressed state in HBM, one warm-up sweep,
-then one profiled sweep (8 chunks x [3 decode + k=4 steps + 2 encode] launches)."""
+then one profiled sweep (8 chunks x [1 decode + k=4 steps + 1 encode] launches for BlockQuant)."""
 import os
 import sys
 
@@ -18,5 +18,13 @@ c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb,
 pl = oocs.Plan(c)
 bench.load_state(pl, nx, ny, nz, 0)
 pl.run(k)
+# the profiled sweep is bracketed by cudaProfilerStart/Stop: run ncu with --profile-from-start off,
+# then -s/-c count launches of this sweep only (chunk 3 of 8 is an interior chunk)
+import torch  # noqa: E402
+
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
 st = pl.run(k)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("sweep ms", st.wall_ms, "launches", list(st.kernel_launches))
