@@ -119,7 +119,7 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def measure_pcie(device, nbytes=256 << 20, reps=3):
+def measure_pcie(device, nbytes=1 << 30, reps=8):
     """Pinned H2D / D2H / duplex bandwidth of THIS box's link (best of `reps`, CUDA events), measured
     before the timed regions, so the e2e PCIe roofline is this box's and not another's (the method of
     tools/measure_box.py, smaller)."""
