@@ -21,14 +21,20 @@ namespace oocs {
 // ---------------------------------------------------------------------------
 // Warp-level 32x32 bit-matrix transpose: lane l holds row l (32 bits); on
 // return lane m holds column m (bit l = bit m of row l).  Five butterfly
-// stages; each is one SHFL, one funnel rotate (SHF.W) by a lane-dependent
-// amount and one LOP3 select -- the per-lane rotate amounts and masks are
-// computed once per kernel.  This is the codec's "warp-level bit-plane
+// stages, each one SHFL plus: for the 16- and 8-bit stages one byte permute
+// (PRMT) with a lane-dependent selector, for the others a funnel rotate (SHF.W)
+// by a lane-dependent amount and one LOP3 select -- the per-lane selectors,
+// rotate amounts and masks are computed once per kernel.  This is the codec's "warp-level bit-plane
 // packing": a block's 64 codes of <= 16 bits become its bit planes in one pass.
 // ---------------------------------------------------------------------------
 struct Xpose {
-    uint32_t rot[5], keep[5];
+    uint32_t rot[5], keep[5];  // stages 2..4 (4-, 2-, 1-bit moves)
+    uint32_t sel[2];           // stages 0, 1 (16- and 8-bit moves): one byte permute each
     __device__ __forceinline__ explicit Xpose(int lane) {
+        // upper lanes keep their low half and take the partner's low half above it; lower lanes the
+        // mirror image: [x0 x1 y0 y1] / [y2 y3 x2 x3] for 16 bits, [x0 y0 x2 y2] / [y1 x1 y3 x3] for 8
+        sel[0] = (lane & 16) == 0 ? 0x5410u : 0x3276u;
+        sel[1] = (lane & 8) == 0 ? 0x6240u : 0x3715u;
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
             const int j = 16 >> s;
@@ -43,6 +49,10 @@ struct Xpose {
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
             const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16 >> s);
+            if (s < 2) {
+                x = __byte_perm(x, y, sel[s]);
+                continue;
+            }
             const uint32_t t = __funnelshift_l(y, y, rot[s]);
             // bitwise mux (keep ? x : t) in one LOP3: lut = (c & a) | (~c & b) = 0xE4
             asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(x) : "r"(x), "r"(t), "r"(keep[s]));
