@@ -97,15 +97,28 @@ def test_codec_on_paper_like_fields_and_identity():
         assert np.array_equal(gpu_decode(raw, 72, 72, 32, 0, 32), arr)
 
 
-def test_encoder_flags_nonfinite():
-    arr = np.ones((4, 8, 8), dtype=np.float32)
-    arr[1, 2, 3] = np.inf
-    ws = to_ws(arr)
-    out = torch.zeros(4 * 2 * 2 * 128, dtype=torch.uint8, device="cuda")
-    err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    oocs.oocs_encode(ws.data_ptr(), out.data_ptr(), 8, 8, 4, oocs.pitch_for(8), 1, 16, err.data_ptr(), stream())
-    torch.cuda.synchronize()
-    assert int(err.item()) == 1
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan, -np.nan, 2.0 ** 126, -(2.0 ** 127)])
+@pytest.mark.parametrize("rate", [8, 16, 24])
+def test_encoder_flags_nonfinite(bad, rate):
+    """a lossy encode of NaN, +-Inf or |x| >= 2^126 raises the error flag -- wherever in the
+    4x4x4 block (every value position, i.e. every lane/row of the warp layout) and in any block of the
+    line; an all-finite input does not."""
+    ax, ay, planes = 40, 8, 4
+    rng = np.random.default_rng(rate)
+    for pos in range(0, 64 * (ax // 4), 7):
+        arr = rng.standard_normal((planes, ay, ax)).astype(np.float32)
+        b, j = divmod(pos, 64)
+        zi, yi, xi = j // 16, (j // 4) % 4, j % 4
+        arr[zi, yi, 4 * b + xi] = bad
+        ws = to_ws(arr)
+        out = torch.zeros(oracle.plane_bytes(ax, ay, 1, rate - 1) * planes, dtype=torch.uint8, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        oocs.oocs_encode(ws.data_ptr(), out.data_ptr(), ax, ay, planes, oocs.pitch_for(ax), 1, rate,
+                         err.data_ptr(), stream())
+        torch.cuda.synchronize()
+        assert int(err.item()) == 1, (bad, pos)
+    arr = rng.standard_normal((planes, ay, ax)).astype(np.float32)
+    gpu_encode(arr, 1, rate)  # asserts the flag stays 0
 
 
 # ----------------------------------------------------------------------------- stencil
