@@ -267,8 +267,10 @@ def cpu_oracle_sample(nx, ny, k, rate, device=None, codec="blockquant"):
 
 
 def threads_used():
-    n = os.environ.get("OMP_NUM_THREADS")
-    return int(n) if n else len(os.sched_getaffinity(0))
+    """Host cores the oracle runs on: every core of the affinity mask.  torchrun exports
+    OMP_NUM_THREADS=1 for its ranks; the oracle legs run on rank 0 alone, so they are widened back to
+    the whole host (oracle.set_threads), and this is the count they actually use."""
+    return len(os.sched_getaffinity(0))
 
 
 # ----------------------------------------------------------------------------- main
@@ -296,6 +298,9 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        import oracle
+
+        oracle.set_threads(threads_used())
         one, cells, sample = cpu_oracle_sample(nx, ny, k, rate,
                                                device="cuda" if torch.cuda.is_available() else None,
                                                codec=args.codec)
@@ -351,12 +356,12 @@ def main():
 
     dt = float(__import__("synth").dt_for())
 
-    def mk(store, mode="swb", codec=None, profile=False, resident_velocity=False):
+    def mk(store, mode="swb", codec=None, profile=False, resident_velocity=False, decoded_velocity=False):
         codec = codec or args.codec
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=codec,
                              rate_bits=rate, mode=mode, store=store, device=local, rank=rank, world=world,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
-                             fusion=args.fuse_encode)
+                             fusion=args.fuse_encode, decoded_velocity=decoded_velocity)
         pl = oocs.Plan(c)
         if world > 1:
             pl.set_exchange((odist.gloo_exchange_fn if gloo else odist.nccl_exchange_fn)(rank, world))
@@ -397,6 +402,17 @@ def main():
                                           if a["kernel_ms"][i] else None} for i in range(3)}}
     gpu_launches = int(sum(a["launches"]))
     clk = clocks.summary()
+    # variant: the read-only velocity kept decoded in HBM (OOCS_FLAG_DECODED_VELOCITY): each chunk decodes
+    # two arrays instead of three; bitwise the same results (tests/test_gpu_parity.py)
+    dv = mk("device", profile=True, decoded_velocity=True)
+    copy_state(dev, dv)
+    per_dv, _ = timed_runs(dv, T, args.steps, args.warmup, barrier)
+    adv = agg(per_dv)
+    dv_ms = allmax(adv["ms"])
+    value_dv = {"value": allsum(adv["cells"]) / (dv_ms * 1e-3) / 1e9, "unit": UNIT,
+                "peak_gpu_mem_gb": dv.info.arena_bytes / 1e9,
+                "decode_GBps": adv["alg"][0] / (adv["kernel_ms"][0] * 1e-3) / 1e9 if adv["kernel_ms"][0] else None}
+    dv.close()
 
     # ---- e2e: compressed state in pinned host memory, PCIe in the timed region -------------
     try:
@@ -476,6 +492,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        oracle.set_threads(threads_used())
         one, cells, sample = cpu_oracle_sample(nx, ny, k, rate, device=f"cuda:{local}", codec=args.codec)
         # repeat the bounded sample until >= 10 s of CPU work (each repeat restarts from the same state)
         secs, reps = 0.0, 0
@@ -485,8 +504,6 @@ def main():
         cpu = {"value": reps * cells / secs / 1e9, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
                "sample": f"{sample}, x{reps}", "seconds": secs}
         # the same oracle on one core, on a quarter-width slab (all cores and 1 core)
-        import oracle
-
         one1, cells1, sample1 = cpu_oracle_sample(nx // 4, ny // 4, k, rate, device=f"cuda:{local}",
                                                   codec=args.codec)
         oracle.set_threads(1)
@@ -504,7 +521,8 @@ def main():
                 "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clk,
                 "peak_gpu_mem_gb": mem_swb / 1e9, "value_store": "device-resident compressed state (HBM)",
-                "value_peak_gpu_mem_gb": mem_dev / 1e9, "host_wall_s": wall, "compare": compare,
+                "value_peak_gpu_mem_gb": mem_dev / 1e9, "value_decoded_velocity_variant": value_dv,
+                "host_wall_s": wall, "compare": compare,
                 "cell_updates_computed_per_useful": a["computed"] / a["cells"]}
         print(json.dumps(line))
     if dist is not None:

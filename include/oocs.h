@@ -120,6 +120,12 @@ typedef enum {
  * LANE_SINGLE_STREAM = one CUDA stream per lane, the literal mapping of Alg. 1's three streams;
  * LANE_SPLIT_STREAMS = a copy and a kernel stream per lane, joined by an event at every switch.  All
  * three execute the same dependencies and produce the same bytes. */
+/* Device store only: keep this rank's velocity (the read-only dataset) decoded in HBM as fp32
+ * (allocated planes x ay x pitch, +4 B per cell) instead of decoding it from the compressed store in
+ * every chunk of every sweep.  The values are the same decode of the same records, so results are
+ * bitwise identical; each chunk's decode then moves two arrays instead of three.  Decoded once per
+ * oocs_load / oocs_store_write_raw of array 0.  Off by default (the compressed-state accounting). */
+#define OOCS_FLAG_DECODED_VELOCITY 64u
 #define OOCS_FLAG_LANE_SINGLE_STREAM 16u
 #define OOCS_FLAG_LANE_SPLIT_STREAMS 32u
 

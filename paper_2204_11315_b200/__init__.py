@@ -44,6 +44,7 @@ FLAG_FUSE_ENCODE = 4
 FLAG_TIMELINE = 8
 FLAG_LANE_SINGLE_STREAM = 16
 FLAG_LANE_SPLIT_STREAMS = 32
+FLAG_DECODED_VELOCITY = 64
 EXECUTOR = {"dispatch": 0, "single": FLAG_LANE_SINGLE_STREAM, "split": FLAG_LANE_SPLIT_STREAMS}
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
 EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY", "NODE"]
@@ -156,7 +157,7 @@ def _check(st: int, where: str):
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
                 device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False,
-                timeline=False, executor="dispatch") -> Config:
+                timeline=False, executor="dispatch", decoded_velocity=False) -> Config:
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -172,7 +173,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.device, c.rank, c.world = device, rank, world
     c.flags = ((FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
                | (FLAG_TIMELINE if timeline else 0) | EXECUTOR[executor]
-               | (FLAG_FUSE_ENCODE if fusion else 0))
+               | (FLAG_FUSE_ENCODE if fusion else 0) | (FLAG_DECODED_VELOCITY if decoded_velocity else 0))
     c.device_capacity = device_capacity
     return c
 

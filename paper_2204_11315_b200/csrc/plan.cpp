@@ -46,6 +46,8 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->device < 0) return bad(err, "bad device ordinal");
     if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
         return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
+    if ((c->flags & OOCS_FLAG_DECODED_VELOCITY) && c->store != OOCS_STORE_DEVICE)
+        return bad(err, "OOCS_FLAG_DECODED_VELOCITY applies to the device store only");
     if (c->schedule < OOCS_SCHED_ALG1 || c->schedule > OOCS_SCHED_DAG_FUNC) return bad(err, "unknown schedule kind");
     if (c->n_lanes != 0 && (c->n_lanes < 2 || c->n_lanes > MAX_LANES)) return bad(err, "n_lanes must be 0 (=3) or 2..8");
     return true;

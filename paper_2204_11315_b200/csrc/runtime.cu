@@ -51,6 +51,7 @@ struct Plan {
     uint8_t *hstore[N_ARRAYS] = {};  // pinned host store, store_planes x plane_bytes per array
     uint8_t *dvel = nullptr;         // OOCS_FLAG_RESIDENT_VELOCITY: compressed velocity kept in HBM
     bool resident_vel = false;
+    float *vdec = nullptr;           // OOCS_FLAG_DECODED_VELOCITY: the rank's velocity decoded (store planes)
     uint8_t *xbuf[4] = {};           // exchange buffers: send_lo, send_hi, recv_lo, recv_hi
     uint64_t xbytes = 0;
     int *d_err = nullptr;
@@ -112,6 +113,11 @@ static inline uint64_t spb(const Plan *p) { return store_pb(p->geo); }
 static inline uint64_t hoff(const Plan *p, int64_t z) { return (uint64_t)(z - p->geo.store_lo) * spb(p); }
 // device store: same indexing
 static inline float *wsa(Plan *p, int set, int a) { return p->ws[set][a]; }
+// velocity of chunk b for the stencil: working-set array 0, or the resident decoded velocity at the
+// chunk's first extent plane (OOCS_FLAG_DECODED_VELOCITY)
+static inline float *vel_of(Plan *p, int set, const oocs_block &b) {
+    return p->vdec ? p->vdec + (b.ext_lo - p->geo.store_lo) * p->geo.pstride : p->ws[set][0];
+}
 
 static cudaEvent_t evt(Plan *p, int kind, int64_t g) { return p->ev[kind][(size_t)(g % (int64_t)p->ev[kind].size())]; }
 
@@ -294,7 +300,7 @@ static void free_plan(Plan *p) {
 // Device arena sizing ("single working buffer" allocator): one pure function shared by
 // oocs_plan_create (which then allocates exactly this) and oocs_plan_estimate (which does not).
 struct Sizes {
-    size_t ws_array = 0, ws_bytes = 0, hfb = 0, staging = 0, arr_store = 0, store_bytes = 0, total = 0;
+    size_t ws_array = 0, ws_bytes = 0, hfb = 0, staging = 0, arr_store = 0, store_bytes = 0, vdec = 0, total = 0;
     uint64_t xbytes = 0;
     bool codec_staging = false, resident_vel = false;
 };
@@ -314,6 +320,10 @@ static Sizes compute_sizes(const Geometry &g) {
     if (!g.host_store) z.total += al(z.arr_store) * 5;  // v + 2x(p_prev, p_curr)
     z.resident_vel = (g.cfg.flags & OOCS_FLAG_RESIDENT_VELOCITY) != 0;
     if (z.resident_vel) z.total += al(z.arr_store);
+    if (g.cfg.flags & OOCS_FLAG_DECODED_VELOCITY) {
+        z.vdec = (size_t)g.store_planes() * g.pstride * 4;
+        z.total += al(z.vdec);
+    }
     if (g.cfg.world > 1) {
         z.xbytes = (uint64_t)2 * g.k * R * store_pb(g);
         z.total += 4 * al(z.xbytes);
@@ -416,6 +426,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
             for (int a = 1; a < N_ARRAYS; ++a) p->dstore[b][a] = (uint8_t *)p->arena.take(arr_store);
     }
     if (p->resident_vel) p->dvel = (uint8_t *)p->arena.take(arr_store);
+    if (z.vdec) p->vdec = (float *)p->arena.take(z.vdec);
     if (g.cfg.world > 1)
         for (int i = 0; i < 4; ++i) p->xbuf[i] = (uint8_t *)p->arena.take(p->xbytes);
     p->d_err = (int *)p->arena.take(sizeof(int));
@@ -612,7 +623,9 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
                 src[a] = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
             dst[a] = wsa(p, w, a);
         }
-        oocs_status r = k_decode(p, src, dst, N_ARRAYS, E, st, stats);
+        // with the velocity kept decoded only the two pressures are decoded
+        const int a0 = p->vdec ? 1 : 0;
+        oocs_status r = k_decode(p, src + a0, dst + a0, N_ARRAYS - a0, E, st, stats);
         if (r) return r;
         break;
     }
@@ -628,13 +641,13 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
             // written back, (level k-1, level k) go straight to S_{t+1}'s records
             void *out_prev = p->dstore[p->cur ^ 1][1] + hoff(p, b.own_lo);
             void *out_curr = p->dstore[p->cur ^ 1][2] + hoff(p, b.own_lo);
-            oocs_status r = k_step_encode(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
+            oocs_status r = k_step_encode(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
                                           hi - b.ext_lo, out_prev, out_curr, st, stats);
             if (r) return r;
             break;
         }
-        oocs_status r = k_step(p, wsa(p, w, 0), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo, st,
-                               stats);
+        oocs_status r = k_step(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo,
+                               st, stats);
         if (r) return r;
         break;
     }
@@ -1049,6 +1062,11 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
                 oocs_status r = k_encode(p, ws, p->dstore[b][array] + hoff(p, z), n, s, nullptr);
                 if (r) return r;
             }
+            if (array == 0 && p->vdec) {  // the resident decoded velocity: decode of the same records
+                oocs_status r = k_decode(p, p->dstore[0][0] + hoff(p, z), p->vdec + (z - g.store_lo) * g.pstride, n,
+                                         s, nullptr);
+                if (r) return r;
+            }
         }
         CU(cudaStreamSynchronize(s));
     }
@@ -1121,6 +1139,12 @@ static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int6
     if (write) {
         for (int b = 0; b < (array == 0 ? 1 : 2); ++b)
             CU(cudaMemcpy(p->dstore[b][array] + off, host, n, cudaMemcpyHostToDevice));
+        if (array == 0 && p->vdec) {
+            oocs_status r = k_decode(p, p->dstore[0][0] + off, p->vdec + (a_lo - R - g.store_lo) * g.pstride,
+                                     a_hi - a_lo, p->lanes[0], nullptr);
+            if (r) return r;
+            CU(cudaStreamSynchronize(p->lanes[0]));
+        }
     } else {
         CU(cudaMemcpy(host, p->dstore[array == 0 ? 0 : p->cur][array] + off, n, cudaMemcpyDeviceToHost));
     }

@@ -41,7 +41,7 @@ def cfg(**kw):
     dict(nx=63), dict(nz=0), dict(n_blocks=17), dict(tb_depth=4), dict(rate_bits=25), dict(rate_bits=1),
     dict(mode="baseline", codec="blockquant"), dict(world=3), dict(rank=4, world=4), dict(dt=-1.0),
     dict(region_sharing=False, store="host"), dict(codec=7), dict(codec="trunc16", rate_bits=8),
-    dict(codec="zfp", rate_bits=33), dict(codec="zfp", rate_bits=0),
+    dict(codec="zfp", rate_bits=33), dict(codec="zfp", rate_bits=0), dict(decoded_velocity=True, store="host"),
 ])
 def test_config_errors(kw):
     with pytest.raises(oocs.OocsError) as e:
@@ -198,6 +198,17 @@ def test_memory_accounting_paper_units(rate):
     if rate == 16:
         assert units["swb"] == pytest.approx(7.5, abs=0.01)  # "0.5x3x3 + 1x3" (P:L245 prints 7.5)
         assert 1 - units["swb"] / units["baseline"] == pytest.approx(1 / 6, abs=1e-3)
+
+
+def test_decoded_velocity_accounting():
+    """OOCS_FLAG_DECODED_VELOCITY adds exactly one fp32 array over the rank's store planes (allocated
+    rows, pitch) to the device-store arena, and nothing else."""
+    kw = dict(nx=1024, ny=1024, nz=1024, dt=0.1, n_blocks=8, tb_depth=4, rate_bits=16, store="device")
+    for world, rank in ((1, 0), (4, 1)):
+        a = oocs.oocs_plan_estimate(cfg(world=world, rank=rank, **kw))
+        b = oocs.oocs_plan_estimate(cfg(world=world, rank=rank, decoded_velocity=True, **kw))
+        planes = a.store_hi - a.store_lo
+        assert b.arena_bytes - a.arena_bytes == _al(planes * a.ay * a.pitch * 4)
 
 
 def test_plan_estimate_c5_swb_vs_dwb():

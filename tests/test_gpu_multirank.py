@@ -25,12 +25,15 @@ def _cuda():
 
 
 def _cfg(nx, ny, nz, n, k, codec, store, mode, rank=0, world=1):
+    dec = store == "device_decv"  # device store with the velocity kept decoded (OOCS_FLAG_DECODED_VELOCITY)
     return oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, codec=codec,
-                            rate_bits=16, mode=mode, store=store, rank=rank, world=world)
+                            rate_bits=16, mode=mode, store="device" if dec else store, rank=rank, world=world,
+                            decoded_velocity=dec)
 
 
 @pytest.mark.parametrize("store,mode,codec", [("host", "swb", "blockquant"), ("device", "swb", "blockquant"),
-                                              ("host", "baseline", "identity"), ("host", "dwb", "identity")])
+                                              ("host", "baseline", "identity"), ("host", "dwb", "identity"),
+                                              ("device_decv", "swb", "blockquant")])
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_equals_single_rank(store, mode, codec, world):
     nx, ny, nz, n, k, T = 32, 40, 128, 8, 2, 6
