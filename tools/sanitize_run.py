@@ -1,5 +1,6 @@
 """Small runs of every hot-path kernel and schedule for compute-sanitizer (memcheck / racecheck /
-synccheck): ragged grids, BlockQuant and ZFP, host and device stores, Alg. 1 and DAG schedules."""
+synccheck): ragged grids, every codec, host and device stores, Alg. 1 and DAG schedules, the resident
+(compressed / decoded) velocity flags and the fused last step + encode."""
 import os
 import sys
 
@@ -13,10 +14,16 @@ R = 4
 nx, ny, nz = 44, 36, 48
 vel, p0 = synth.fields(nx, ny, nz)
 az = nz + 2 * R
-for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("identity", 32)):
-    for store, sched, mode in (("host", "alg1", "swb"), ("device", "alg1", "swb"), ("host", "dag_func", "dwb")):
+for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("trunc16", 16), ("identity", 32)):
+    for store, sched, mode, extra in (("host", "alg1", "swb", {}), ("device", "alg1", "swb", {}),
+                                      ("host", "dag_func", "dwb", {}),
+                                      ("device", "alg1", "swb", {"decoded_velocity": True}),
+                                      ("device", "alg1", "swb", {"decoded_velocity": True, "fusion": True}),
+                                      ("host", "alg1", "swb", {"resident_velocity": True})):
+        if extra.get("fusion") and codec != "blockquant":
+            continue
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=3, tb_depth=2, codec=codec,
-                             rate_bits=rate, mode=mode, store=store, schedule=sched)
+                             rate_bits=rate, mode=mode, store=store, schedule=sched, **extra)
         pl = oocs.Plan(c)
         for a, arr in enumerate((vel, p0, p0)):
             pl.load(a, arr, 0, az)
@@ -24,4 +31,4 @@ for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("ident
         out = pl.store(2, 0, az)
         assert np.isfinite(out).all()
         pl.close()
-        print("ok", codec, rate, store, sched, mode, flush=True)
+        print("ok", codec, rate, store, sched, mode, extra, flush=True)
