@@ -49,7 +49,7 @@ def env_int(k, d):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)  # >= 5 timed repetitions
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="oocs", choices=["oocs", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
@@ -214,6 +214,12 @@ class _Null:
 
     def __exit__(self, *a):
         pass
+
+
+def step_summary(stats_list):
+    """Per timed step device ms (median and best of the repetitions, with all of them)."""
+    ms = sorted(s.wall_ms for s in stats_list)
+    return {"median": float(np.median(ms)), "best": ms[0], "all": [round(s.wall_ms, 3) for s in stats_list]}
 
 
 def agg(stats_list):
@@ -522,6 +528,7 @@ def main():
                 "gpu_launches": gpu_launches, "clocks": clk,
                 "peak_gpu_mem_gb": mem_swb / 1e9, "value_store": "device-resident compressed state (HBM)",
                 "value_peak_gpu_mem_gb": mem_dev / 1e9, "value_decoded_velocity_variant": value_dv,
+                "step_ms_rank0": {"value": step_summary(per), "e2e": step_summary(per_h)},
                 "host_wall_s": wall, "compare": compare,
                 "cell_updates_computed_per_useful": a["computed"] / a["cells"]}
         print(json.dumps(line))

@@ -12,5 +12,6 @@ tail -2 gpurun_out/launches.log
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:stencil_step -s 12 -c 1 -o gpurun_out/prof_step python tools/profile_kernels.py > gpurun_out/prof_step.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:bq_decode -s 3 -c 1 -o gpurun_out/prof_dec python tools/profile_kernels.py > gpurun_out/prof_dec.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:bq_encode -s 3 -c 1 -o gpurun_out/prof_enc python tools/profile_kernels.py > gpurun_out/prof_enc.log 2>&1
-tail -2 gpurun_out/prof_enc.log
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:stencil_step -s 15 -c 1 -o gpurun_out/prof_fused python tools/profile_kernels.py --fuse > gpurun_out/prof_fused.log 2>&1
+tail -2 gpurun_out/prof_enc.log gpurun_out/prof_fused.log
 ls gpurun_out
