@@ -119,6 +119,17 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def smi_mem_used_mib(device):
+    """Device memory in use (MiB) per nvidia-smi: the cross-check of a plan's arena bytes (SURVEY 8(d):
+    arena bytes + NVML memory.used delta).  None when nvidia-smi is unavailable."""
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(device), "--query-gpu=memory.used",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20).stdout
+        return int(out.strip().splitlines()[0])
+    except Exception:
+        return None
+
+
 def measure_pcie(device, nbytes=1 << 30, reps=8):
     """Pinned H2D / D2H / duplex bandwidth of THIS box's link (best of `reps`, CUDA events), measured
     before the timed regions, so the e2e PCIe roofline is this box's and not another's (the method of
@@ -426,7 +437,11 @@ def main():
     except Exception as exc:  # the committed measurement stands in (reported as such)
         print(f"bench: live PCIe probe failed ({exc}); using profiles/r01_measure_box.json", file=sys.stderr)
         pcie_live = None
+    torch.cuda.synchronize(local)
+    smi0 = smi_mem_used_mib(local)
     host = mk("host")
+    smi1 = smi_mem_used_mib(local)
+    smi_delta_gb = (smi1 - smi0) * 2**20 / 1e9 if smi0 is not None and smi1 is not None else None
     copy_state(dev, host)
     dev.close()
     per_h, wall_h = timed_runs(host, T, args.steps, args.warmup, barrier)
@@ -526,7 +541,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clk,
-                "peak_gpu_mem_gb": mem_swb / 1e9, "value_store": "device-resident compressed state (HBM)",
+                "peak_gpu_mem_gb": mem_swb / 1e9, "peak_gpu_mem_smi_delta_gb": smi_delta_gb,
+                "value_store": "device-resident compressed state (HBM)",
                 "value_peak_gpu_mem_gb": mem_dev / 1e9, "value_decoded_velocity_variant": value_dv,
                 "step_ms_rank0": {"value": step_summary(per), "e2e": step_summary(per_h)},
                 "host_wall_s": wall, "compare": compare,
