@@ -118,3 +118,20 @@ def test_zfp_pipeline_equals_injected_roundtrip(store, sched, rate, k):
         pp_b, pc_b = gpu_encode(pp, rate), gpu_encode(pc, rate)
         pp, pc = gpu_decode(pp_b, ax, ay, az, rate), gpu_decode(pc_b, ax, ay, az, rate)
     assert np.array_equal(got[0], pp_b) and np.array_equal(got[1], pc_b)
+
+
+def test_zfp_gpu_matches_hand_derived_golden_records():
+    """The GPU encoder against the records derived by hand in docs/FORMAT.md §4.1
+    (tests/golden/zfp_blocks.txt), independently of the oracle: each golden block is placed at every
+    position of a 4-plane slab of 3 x 3 blocks, encoded, and every record compared; decode is exact."""
+    from test_oracle_zfp import golden_zfp_records
+
+    for name, rate, x, want in golden_zfp_records():
+        blk = x.reshape(4, 4, 4)  # (zi, yi, xi)
+        arr = np.ascontiguousarray(np.tile(blk, (1, 3, 3)), dtype=np.float32)  # 4 planes x 12 x 12
+        got = gpu_encode(arr, rate)
+        rec = 8 * rate
+        for i in range(9):
+            assert got[i * rec:(i + 1) * rec].tobytes() == want, (name, rate, i)
+        dec = gpu_decode(got, 12, 12, 4, rate)
+        assert np.array_equal(dec.view(np.uint32), arr.view(np.uint32)), (name, rate)

@@ -147,3 +147,69 @@ def test_incore_zero_steps_identity_and_determinism():
     s6p, s6c = oracle.incore(vel, p0.copy(), p0.copy(), 0.1, 6)
     oracle.step(vel, s5p, s5c, 0.1, R, shp[0] - R)
     assert np.array_equal(s5p, s6c)
+
+
+# ---- non-uniform velocity: the c = (v dt)^2 factor is taken at the updated cell -----------------------
+def test_bruteforce_25_terms_nonuniform_velocity():
+    """Random fields and a strongly varying random velocity: every updated cell against the 25-term sum
+    written out with exact rationals from the fp32 inputs (p_next = 2p - p_prev + v^2 dt^2 Lap25),
+    rounded once to fp32.  A velocity taken at a neighbour, c = v^2 dt or c = v dt^2 all fail."""
+    rng = np.random.default_rng(11)
+    shp = _grid(5, 4, 3)
+    vel = rng.uniform(0.5, 3.0, size=shp).astype(np.float32)
+    pc = rng.normal(size=shp).astype(np.float32)
+    pp = rng.normal(size=shp).astype(np.float32)
+    dt = np.float32(0.13)
+    out = pp.copy()
+    oracle.step(vel, out, pc, dt, R, shp[0] - R)
+    coef = [Fraction(-205, 72), Fraction(8, 5), Fraction(-1, 5), Fraction(8, 315), Fraction(-1, 560)]
+    F = lambda a: Fraction(float(a))
+    n_checked = 0
+    for z in range(R, shp[0] - R):
+        for y in range(R, shp[1] - R):
+            for x in range(R, shp[2] - R):
+                lap = 3 * coef[0] * F(pc[z, y, x])
+                for m in range(1, 5):
+                    lap += coef[m] * (F(pc[z, y, x + m]) + F(pc[z, y, x - m]) + F(pc[z, y + m, x]) + F(pc[z, y - m, x])
+                                      + F(pc[z + m, y, x]) + F(pc[z - m, y, x]))
+                c = (F(vel[z, y, x]) * F(dt)) ** 2
+                want = 2 * F(pc[z, y, x]) - F(pp[z, y, x]) + c * lap
+                got = F(out[z, y, x])
+                # the oracle rounds its fp64 sum once to fp32: within one fp32 ulp of the exact value
+                ulp = np.spacing(np.float32(abs(float(want))))
+                assert abs(float(got - want)) <= float(ulp), (z, y, x, float(got), float(want))
+                # and distinguishable from the plausible mistakes
+                wrong_c = [(F(wv) * F(dt)) ** 2 for wv in (vel[z, y, x + 1], vel[z + 1, y, x], vel[z, y - 1, x])]
+                wrong_c += [F(vel[z, y, x]) ** 2 * F(dt), F(vel[z, y, x]) * F(dt) ** 2]
+                for wc in wrong_c:
+                    if abs(float((wc - c) * lap)) > 4 * float(ulp):
+                        assert abs(float(got - (2 * F(pc[z, y, x]) - F(pp[z, y, x]) + wc * lap))) > float(ulp)
+                n_checked += 1
+    assert n_checked == 5 * 4 * 3
+
+
+def test_quadratic_field_closed_form_with_varying_velocity():
+    """f = x^2+y^2+z^2, p_-1 = p_0 = f, and a velocity with v^2 linear in x, y and z (so that
+    c = (v dt)^2 is linear and Lap25 c = 0, the stencil being exact to degree 9): then
+    p_n = f + 3 n (n+1) c(x,y,z) pointwise, on cells at distance >= nR from the fixed boundary.
+    With c varying by ~3e-3 per plane a velocity index off by one cell in any axis is ~10^3 ulps off."""
+    nx = ny = nz = 36
+    shp = _grid(nx, ny, nz)
+    z, y, x = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in shp], indexing="ij")
+    f = ((x - shp[2] / 2) ** 2 + (y - shp[1] / 2) ** 2 + (z - shp[0] / 2) ** 2).astype(np.float32)
+    vel = np.sqrt(1.0 + 0.5 * z + 0.3 * x + 0.2 * y).astype(np.float32)
+    dt = np.float32(0.05)
+    c = (vel.astype(np.float64) * float(dt)) ** 2  # exactly the oracle's c (fp64 from fp32 v, dt)
+    assert vel.max() * float(dt) < 0.4529  # CFL (DESIGN.md Q1)
+    p_prev, p_curr = f.copy(), f.copy()
+    steps = 3
+    oracle.incore(vel, p_prev, p_curr, dt, steps)
+    d = steps * R
+    sl = (slice(R + d, shp[0] - R - d), slice(R + d, shp[1] - R - d), slice(R + d, shp[2] - R - d))
+    for n, got in ((steps, p_curr), (steps - 1, p_prev)):
+        want = f.astype(np.float64) + 3 * n * (n + 1) * c
+        np.testing.assert_allclose(got[sl], want[sl], rtol=3e-7, atol=0)
+        # c shifted by one cell along any axis is far outside that tolerance
+        for ax_ in range(3):
+            wrong = f.astype(np.float64) + 3 * n * (n + 1) * np.roll(c, 1, axis=ax_)
+            assert np.max(np.abs(got[sl] - wrong[sl]) / np.abs(wrong[sl])) > 1e-5, (n, ax_)

@@ -134,3 +134,36 @@ def test_zfp_pipeline_equals_incore_with_injected_roundtrip(r, n, k):
         pp, pc = rt(pp), rt(pc)
     assert np.array_equal(oracle.decode_planes(Sp, ax, ay, az, C, r), pp)
     assert np.array_equal(oracle.decode_planes(Sc, ax, ay, az, C, r), pc)
+
+
+# ---- golden records derived by hand from zfp's published algorithm (docs/FORMAT.md §4) -------------
+def _golden_values(name):
+    j = np.arange(64)
+    return {"zero": np.zeros(64), "const_p1": np.ones(64), "const_m1": -np.ones(64),
+            "ramp_x": (j % 4).astype(np.float64), "ramp_y": ((j // 4) % 4).astype(np.float64)}[name].astype(np.float32)
+
+
+def golden_zfp_records():
+    """(name, rate, values, expected record bytes) from tests/golden/zfp_blocks.txt."""
+    import os
+    out = []
+    path = os.path.join(os.path.dirname(__file__), "golden", "zfp_blocks.txt")
+    for line in open(path):
+        if not line.strip() or line.startswith("#"):
+            continue
+        f = line.split()
+        name, rate = f[0], int(f[1])
+        word0 = int(next(t for t in f if t.startswith("0x")), 16)
+        rec = np.zeros(rate, dtype=np.uint64)
+        rec[0] = word0
+        out.append((name, rate, _golden_values(name), rec.tobytes()))
+    return out
+
+
+@pytest.mark.parametrize("name,rate,x,want", golden_zfp_records(), ids=lambda v: str(v)[:12])
+def test_golden_records_hand_derived(name, rate, x, want):
+    # header 2e+1 (9 bits, e = emax + 127), one DC (and one first-order) coefficient in negabinary,
+    # group tests / unary run lengths per bit plane from plane 31 down, truncated at 64*rate bits
+    assert oracle.zfp_encode_block(x, rate) == want, name
+    # every golden block is exactly representable: decoding returns the input bit for bit
+    assert np.array_equal(oracle.zfp_decode_block(want, rate).view(np.uint32), x.view(np.uint32)), name
