@@ -63,7 +63,7 @@ typedef enum {
     OOCS_ERR_DATA = 6,       /* NaN/Inf or |x| >= 2^126 given to a lossy codec */
     OOCS_ERR_HOST_OOM = 7,   /* host (pinned) allocation failed */
     OOCS_ERR_CUDA = 8,       /* CUDA runtime error; plan poisoned */
-    OOCS_ERR_EXCHANGE = 9,   /* the multi-GPU halo exchange callback failed */
+    OOCS_ERR_EXCHANGE = 9,   /* multi-GPU: peers not connected, or a peer handle that cannot be opened */
     OOCS_ERR_STATE = 10      /* plan poisoned by an earlier failure, or call out of order */
 } oocs_status;
 
@@ -108,7 +108,7 @@ typedef enum {
  * 35% fewer HBM bytes than step + encode but is issue-bound and measures ~1.5%
  * slower on B200.  Ignored by other modes. */
 #define OOCS_FLAG_FUSE_ENCODE 4u
-/* Record a CUDA-event span around every work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) of a
+/* Record a CUDA-event span around every work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, SEND) of a
  * run; read it back with oocs_timeline (the analog of the paper's pipeline figures fig:pipe1 /
  * fig:newbot).  Costs two event records per op. */
 #define OOCS_FLAG_TIMELINE 8u
@@ -203,7 +203,7 @@ typedef struct {
  * finished it (end), in ms from the run's first event.  A copy's start is when its stream issued it; it
  * may then queue behind another lane's copy on the same DMA engine. */
 typedef struct {
-    int32_t kind;  /* oocs_op_kind (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) */
+    int32_t kind;  /* oocs_op_kind (H2D, CARRY, DECODE, STEP, ENCODE, D2H, SEND) */
     int32_t lane;
     int64_t g;     /* global block counter */
     int32_t block;
@@ -217,7 +217,7 @@ typedef struct {
 typedef enum {
     OOCS_OP_H2D = 0, OOCS_OP_CARRY = 1, OOCS_OP_DECODE = 2, OOCS_OP_STEP = 3,
     OOCS_OP_ENCODE = 4, OOCS_OP_D2H = 5, OOCS_OP_RECORD = 6, OOCS_OP_WAIT = 7,
-    OOCS_OP_EXCHANGE = 8
+    OOCS_OP_SEND = 8 /* multi-GPU: an edge chunk's kR encoded planes straight into the neighbour's ghost slot */
 } oocs_op_kind;
 
 typedef enum {
@@ -228,16 +228,6 @@ typedef enum {
     OOCS_EV_CARRY = 4, /* BASELINE mode: carry of block g copied into its working buffer */
     OOCS_EV_NODE = 5   /* DAG schedules: completion of DAG node ev_g (index in the schedule's node list) */
 } oocs_event_kind;
-
-/* Multi-GPU halo exchange, called by oocs_run on the host after sweep
- * `sweep` has been fully written back.  send_lo/recv_lo (send_hi/recv_hi)
- * are DEVICE pointers to k*R compressed planes x 2 pressure arrays destined
- * for / arriving from rank-1 (rank+1); NULL at the domain edge.  The callback
- * must complete the transfer (e.g. NCCL send/recv on `stream`, then
- * synchronize) before returning 0; non-zero aborts the run with
- * OOCS_ERR_EXCHANGE. */
-typedef int (*oocs_exchange_fn)(void *user, int64_t sweep, void *send_lo, void *send_hi,
-                                void *recv_lo, void *recv_hi, uint64_t bytes, void *stream);
 
 typedef struct oocs_plan oocs_plan;
 
@@ -285,8 +275,34 @@ oocs_status oocs_plan_create_in(const oocs_config *cfg, void *arena, uint64_t ar
 
 oocs_status oocs_plan_query(const oocs_plan *plan, oocs_plan_info *info);
 
-/* Install the halo-exchange callback (required when world > 1). */
-oocs_status oocs_set_exchange(oocs_plan *plan, oocs_exchange_fn fn, void *user);
+/* ---- multi-GPU: z-slab sharding with a peer-memory halo exchange -----------------
+ * Rank r of `world` owns a contiguous run of whole chunks.  The kR pressure planes it needs beyond its
+ * slab (the neighbours' edge planes of S_t, P:L85 temporal-blocking halo) arrive in HBM "ghost slots"
+ * (two per side, by parity of the sweep's state index), written directly by the neighbour over
+ * NVLink (CUDA IPC peer memory; the same GPU when ranks share one): right after the neighbour's edge
+ * chunk is encoded, a copy kernel on that chunk's stream stores its kR compressed planes into our
+ * slot and then writes a sequence number into our READY flag (cuStreamWriteValue32, fenced).  Our
+ * edge chunk's decode waits for that number on its own stream (cuStreamWaitValue32) and, once it has
+ * read the slot, writes the neighbour's FREE flag so the slot can be reused two sweeps later.  No
+ * host synchronisation, no drain between sweeps, no re-streaming of halos over PCIe: the multi-GPU
+ * analogue of region sharing.  The static velocity ghosts are loaded once.
+ *
+ * Protocol: every rank calls oocs_peer_handle, the caller moves the blobs between processes (e.g.
+ * torch.distributed all_gather_object: plumbing only), every rank calls oocs_peer_connect with its
+ * neighbours' blobs.  Runs of all ranks must advance by the same steps; load/store/raw calls and
+ * oocs_destroy must not overlap a neighbour's oocs_run (a barrier between them is the caller's).
+ * The ranks may live in one process (same-process peers use plain pointers) or in several. */
+#define OOCS_PEER_HANDLE_BYTES 256
+
+/* Fill `out` (OOCS_PEER_HANDLE_BYTES, host memory) with this plan's exchange-region handle.
+ * Errors: OOCS_ERR_STATE (world == 1: no exchange region), OOCS_ERR_CUDA. */
+oocs_status oocs_peer_handle(const oocs_plan *plan, void *out);
+
+/* Map the neighbours' exchange regions: `lower` = rank-1's handle (NULL for rank 0), `upper` = rank+1's
+ * (NULL for the last rank).  Validates that the blobs come from the same job geometry.
+ * Errors: OOCS_ERR_CONFIG (wrong / mismatched blob, missing neighbour), OOCS_ERR_EXCHANGE (IPC open
+ * failed), OOCS_ERR_STATE. */
+oocs_status oocs_peer_connect(oocs_plan *plan, const void *lower, const void *upper);
 
 /* NULL-safe; frees streams, events, arena and pinned store. */
 oocs_status oocs_destroy(oocs_plan *plan);
@@ -306,6 +322,11 @@ oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t 
  * (same layout as oocs_load). */
 oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi);
 
+/* The same two calls with DEVICE memory of the plan's device on the caller's side (same raw layout):
+ * state generated or consumed on the GPU never crosses PCIe uncompressed. */
+oocs_status oocs_load_device(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi);
+oocs_status oocs_store_device(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi);
+
 /* Raw compressed bytes of allocated planes [a_lo, a_hi) of one array,
  * to / from HOST memory (bitstream parity tests, checkpoints). */
 oocs_status oocs_store_read_raw(oocs_plan *plan, int32_t array, void *dst, int64_t a_lo, int64_t a_hi);
@@ -316,7 +337,7 @@ oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src
  * of Algorithm 1 over this rank's blocks, sweeps pipelined back to back.
  * Blocks the host until the device work is complete.  `out` may be NULL.
  * Errors: OOCS_ERR_CONFIG (steps), OOCS_ERR_DATA (encoder rejected a value;
- * state undefined), OOCS_ERR_CUDA, OOCS_ERR_EXCHANGE, OOCS_ERR_STATE. */
+ * state undefined), OOCS_ERR_CUDA, OOCS_ERR_EXCHANGE (world > 1 and not connected), OOCS_ERR_STATE. */
 oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out);
 
 /* Spans of the last oocs_run made with OOCS_FLAG_TIMELINE, in schedule order.  Copies min(cap, n)

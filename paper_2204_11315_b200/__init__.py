@@ -21,9 +21,9 @@ import numpy as np
 __all__ = [
     "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
     "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
-    "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_store_read_raw",
+    "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_load_device", "oocs_store_device", "oocs_store_read_raw",
     "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
-    "oocs_set_exchange", "Plan", "XOFF", "pitch_for",
+    "oocs_peer_handle", "oocs_peer_connect", "PEER_HANDLE_BYTES", "Plan", "XOFF", "pitch_for",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -46,7 +46,8 @@ FLAG_LANE_SINGLE_STREAM = 16
 FLAG_LANE_SPLIT_STREAMS = 32
 FLAG_DECODED_VELOCITY = 64
 EXECUTOR = {"dispatch": 0, "single": FLAG_LANE_SINGLE_STREAM, "split": FLAG_LANE_SPLIT_STREAMS}
-OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "EXCHANGE"]
+OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "SEND"]
+PEER_HANDLE_BYTES = 256
 EV_KINDS = ["H2D", "DEC", "ENC", "D2H", "CARRY", "NODE"]
 
 i32, i64, u32, u64, f32, f64, vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
@@ -98,9 +99,6 @@ class Span(ctypes.Structure):
                 ("pad", i32), ("start_ms", f64), ("end_ms", f64), ("host_ms", f64)]
 
 
-EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, vp, i64, vp, vp, vp, vp, u64, vp)
-
-
 class OocsError(RuntimeError):
     def __init__(self, status: int, where: str, msg: str):
         super().__init__(f"{where}: OOCS_ERR_{STATUS.get(status, status)}: {msg}")
@@ -126,9 +124,12 @@ def lib():
             "oocs_plan_create_in": ([P(Config), vp, u64, P(vp)], i32),
             "oocs_plan_query": ([vp, P(PlanInfo)], i32),
             "oocs_plan_estimate": ([P(Config), P(PlanInfo)], i32),
-            "oocs_set_exchange": ([vp, EXCHANGE_FN, vp], i32),
+            "oocs_peer_handle": ([vp, vp], i32),
+            "oocs_peer_connect": ([vp, vp, vp], i32),
             "oocs_destroy": ([vp], i32),
             "oocs_load": ([vp, i32, vp, i64, i64], i32),
+            "oocs_load_device": ([vp, i32, vp, i64, i64], i32),
+            "oocs_store_device": ([vp, i32, vp, i64, i64], i32),
             "oocs_store": ([vp, i32, vp, i64, i64], i32),
             "oocs_store_read_raw": ([vp, i32, vp, i64, i64], i32),
             "oocs_store_write_raw": ([vp, i32, vp, i64, i64], i32),
@@ -244,6 +245,16 @@ def oocs_load(h, array: int, src: np.ndarray, a_lo: int, a_hi: int):
     _check(lib().oocs_load(h, array, _ptr(src), a_lo, a_hi), "oocs_load")
 
 
+def oocs_load_device(h, array: int, src_ptr: int, a_lo: int, a_hi: int):
+    """src_ptr: DEVICE pointer to (a_hi-a_lo, ay, ax) float32 on the plan's device."""
+    _check(lib().oocs_load_device(h, array, src_ptr, a_lo, a_hi), "oocs_load_device")
+
+
+def oocs_store_device(h, array: int, dst_ptr: int, a_lo: int, a_hi: int):
+    """dst_ptr: DEVICE pointer to (a_hi-a_lo, ay, ax) float32 on the plan's device."""
+    _check(lib().oocs_store_device(h, array, dst_ptr, a_lo, a_hi), "oocs_store_device")
+
+
 def oocs_store(h, array: int, dst: np.ndarray, a_lo: int, a_hi: int):
     assert dst.dtype == np.float32
     _check(lib().oocs_store(h, array, _ptr(dst), a_lo, a_hi), "oocs_store")
@@ -274,8 +285,18 @@ def oocs_timeline(h):
                  start_ms=s.start_ms, end_ms=s.end_ms, host_ms=s.host_ms) for s in arr]
 
 
-def oocs_set_exchange(h, fn, user=None):
-    _check(lib().oocs_set_exchange(h, fn, user), "oocs_set_exchange")
+def oocs_peer_handle(h) -> bytes:
+    """This rank's exchange-region handle (multi-GPU, world > 1): PEER_HANDLE_BYTES opaque bytes."""
+    buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+    _check(lib().oocs_peer_handle(h, buf), "oocs_peer_handle")
+    return buf.raw
+
+
+def oocs_peer_connect(h, lower: bytes | None, upper: bytes | None):
+    """Map rank-1's (lower) and rank+1's (upper) exchange regions; None at the domain edges."""
+    lo = ctypes.create_string_buffer(lower, PEER_HANDLE_BYTES) if lower is not None else None
+    up = ctypes.create_string_buffer(upper, PEER_HANDLE_BYTES) if upper is not None else None
+    _check(lib().oocs_peer_connect(h, lo, up), "oocs_peer_connect")
 
 
 # ---- kernel-level calls on caller device memory (integer device pointers) ---------
@@ -307,10 +328,18 @@ class Plan:
         else:
             self.handle = oocs_plan_create(self.cfg)
         self.info = oocs_plan_query(self.handle)
-        self._cb = None
 
     def load(self, array, src, a_lo, a_hi):
         oocs_load(self.handle, array, src, a_lo, a_hi)
+
+    def load_device(self, array, tensor, a_lo, a_hi):
+        """tensor: contiguous float32 CUDA tensor (a_hi-a_lo, ay, ax) on the plan's device."""
+        assert tensor.is_cuda and tensor.is_contiguous() and tuple(tensor.shape) == (a_hi - a_lo, self.info.ay, self.info.ax)
+        oocs_load_device(self.handle, array, tensor.data_ptr(), a_lo, a_hi)
+
+    def store_device(self, array, tensor, a_lo, a_hi):
+        assert tensor.is_cuda and tensor.is_contiguous() and tuple(tensor.shape) == (a_hi - a_lo, self.info.ay, self.info.ax)
+        oocs_store_device(self.handle, array, tensor.data_ptr(), a_lo, a_hi)
 
     def store(self, array, a_lo, a_hi):
         out = np.empty((a_hi - a_lo, self.info.ay, self.info.ax), dtype=np.float32)
@@ -331,17 +360,11 @@ class Plan:
     def timeline(self):
         return oocs_timeline(self.handle)
 
-    def set_exchange(self, pyfn):
-        """pyfn(sweep, send_lo, send_hi, recv_lo, recv_hi, nbytes, stream) -> int (device pointers as ints)."""
-        def _tramp(user, sweep, sl, sh, rl, rh, nbytes, stream):
-            try:
-                return int(pyfn(sweep, sl, sh, rl, rh, nbytes, stream) or 0)
-            except Exception:  # never let a Python exception cross the C ABI
-                import traceback
-                traceback.print_exc()
-                return 1
-        self._cb = EXCHANGE_FN(_tramp)
-        oocs_set_exchange(self.handle, self._cb)
+    def peer_handle(self) -> bytes:
+        return oocs_peer_handle(self.handle)
+
+    def peer_connect(self, lower, upper):
+        oocs_peer_connect(self.handle, lower, upper)
 
     def close(self):
         if self.handle is not None:

@@ -1227,6 +1227,47 @@ cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU halo send: two (src, dst) byte ranges of the same length, dst in a neighbour's HBM mapped
+// through CUDA IPC (NVLink peer stores) -- SM-driven so the copy engines stay free for the PCIe
+// pipeline.  16-byte vectors when every pointer and the length allow it, else 8-byte.
+// ---------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) peer_copy_kernel(const V *__restrict__ s0, V *__restrict__ d0,
+                                                        const V *__restrict__ s1, V *__restrict__ d1, uint64_t n) {
+    const V *s = blockIdx.y ? s1 : s0;
+    V *d = blockIdx.y ? d1 : d0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+        V v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i + j * stride < n) v[j] = __ldcs(s + i + j * stride);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i + j * stride < n) d[i + j * stride] = v[j];
+    }
+}
+
+cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, void *dst1, uint64_t bytes,
+                             cudaStream_t st) {
+    if (!bytes) return cudaSuccess;
+    const uintptr_t all = reinterpret_cast<uintptr_t>(src0) | reinterpret_cast<uintptr_t>(dst0) |
+                          reinterpret_cast<uintptr_t>(src1) | reinterpret_cast<uintptr_t>(dst1) | (uintptr_t)bytes;
+    if (all & 7) return cudaErrorInvalidValue;
+    const bool v16 = (all & 15) == 0;
+    const uint64_t n = bytes / (v16 ? 16 : 8);
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(148, (n + 1023) / 1024));
+    const dim3 grid(gx, 2);
+    if (v16)
+        peer_copy_kernel<uint4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(src0), static_cast<uint4 *>(dst0),
+                                                       static_cast<const uint4 *>(src1), static_cast<uint4 *>(dst1), n);
+    else
+        peer_copy_kernel<uint2><<<grid, 256, 0, st>>>(static_cast<const uint2 *>(src0), static_cast<uint2 *>(dst0),
+                                                       static_cast<const uint2 *>(src1), static_cast<uint2 *>(dst1), n);
+    return cudaGetLastError();
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency,
 // so the library still loads on a CPU-only box)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,

@@ -51,6 +51,10 @@ cudaError_t launch_step_encode(const float *vel, const float *pprev, const float
                                int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
                                void *out_prev, void *out_curr, int *err, cudaStream_t st);
 
+// multi-GPU halo send: two equal-length byte ranges (8-byte multiples), dst possibly peer memory
+cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, void *dst1, uint64_t bytes,
+                             cudaStream_t st);
+
 void set_error(const std::string &msg);
 
 }  // namespace oocs

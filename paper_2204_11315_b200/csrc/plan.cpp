@@ -43,6 +43,8 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->nz / 4 < c->n_blocks) return bad(err, "more chunks than 4-plane units: empty chunk (S:L57)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad(err, "bad rank/world");
     if (c->n_blocks % c->world) return bad(err, "world must divide n_blocks (whole chunks per GPU)");
+    if (c->world > 1 && c->mode == OOCS_MODE_BASELINE)
+        return bad(err, "the uncompressed BASELINE (fig:3ver(a)) is a single-GPU comparison: world must be 1");
     if (c->device < 0) return bad(err, "bad device ordinal");
     if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
         return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
@@ -102,8 +104,8 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
     }
     g->b_lo = (int)((int64_t)c.rank * n / c.world);
     g->b_hi = (int)((int64_t)(c.rank + 1) * n / c.world);
-    // a rank's first chunk has no predecessor on this GPU: its whole extent crosses PCIe
-    // (the halo below it arrives in the ghost planes through the exchange)
+    // a rank's first chunk has no predecessor on this GPU: no carry (its pressure halo below the slab
+    // arrives in a ghost slot from rank-1, its velocity halo is in the store)
     oocs_block &first = g->blocks[g->b_lo];
     first.carry_lo = first.carry_hi = first.body_lo = first.ext_lo;
     g->store_lo = std::max<int64_t>(-R, g->blocks[g->b_lo].own_lo - kR);
@@ -158,19 +160,29 @@ struct Emitter {
 };
 }  // namespace
 
+// multi-GPU: which of a chunk's edges go to a neighbour's ghost slot after its encode (bit 0: its first
+// kR owned planes to rank-1, bit 1: its last kR owned planes to rank+1)
+static int send_mask(const Geometry &geo, int blk) {
+    int m = 0;
+    if (geo.cfg.world > 1) {
+        if (blk == geo.b_lo && geo.cfg.rank > 0) m |= 1;
+        if (blk == geo.b_hi - 1 && geo.cfg.rank + 1 < geo.cfg.world) m |= 2;
+    }
+    return m;
+}
+
 static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
     ops.clear();
     Emitter E{ops};
     const int nb = geo.nb();
     const int64_t G = sweeps * nb;
-    const bool multi = geo.cfg.world > 1;
     if (!geo.host_store) {
         for (int64_t g = 0; g < G; ++g) {
             const int t = (int)(g / nb), blk = geo.b_lo + (int)(g % nb);
             E.emit(OOCS_OP_DECODE, 0, g, blk, t);
             for (int s = 1; s <= geo.k; ++s) E.emit(OOCS_OP_STEP, 0, g, blk, t, s);
             E.emit(OOCS_OP_ENCODE, 0, g, blk, t);
-            if (multi && g % nb == nb - 1 && t + 1 < sweeps) E.emit(OOCS_OP_EXCHANGE, 0, g, blk, t);
+            if (const int m = send_mask(geo, blk)) E.emit(OOCS_OP_SEND, 0, g, blk, t, m);
         }
         return;
     }
@@ -194,8 +206,7 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         for (int64_t g = 0; g < G; ++g) {
             const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
             const oocs_block &b = geo.blocks[blk];
-            if (multi && i == 0 && t > 0) E.emit(OOCS_OP_EXCHANGE, s, g, blk, t - 1);
-            else raw_waits(g, b.body_lo, b.body_hi);
+            raw_waits(g, b.body_lo, b.body_hi);
             E.emit(OOCS_OP_H2D, s, g, blk, t);
             if (i > 0) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_CARRY, g);
             if (i + 1 < nb) {  // the next chunk's working set was last used by chunk g+1-L
@@ -218,10 +229,12 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         if (carry_ev >= 0) E.emit(OOCS_OP_WAIT, s, p, blk, t, OOCS_EV_CARRY, carry_ev);
         E.emit(OOCS_OP_ENCODE, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_ENC, p);
+        // multi-GPU: the edge planes go to the neighbour's ghost slot straight from the encoded buffer,
+        // before the D2H (the neighbour's edge chunk is waiting for them)
+        if (const int m = send_mask(geo, blk)) E.emit(OOCS_OP_SEND, s, p, blk, t, m);
         E.emit(OOCS_OP_D2H, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_D2H, p);
     };
-    bool synced = false;  // an EXCHANGE drained every lane: no cross-sweep waits needed
     for (int64_t g = 0; g < G; ++g) {
         const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
         const oocs_block &b = geo.blocks[blk];
@@ -235,8 +248,7 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
             tail(pending, carry ? g : -1);
             pending = -1;
         }
-        if (!synced) raw_waits(g, b.body_lo, b.body_hi);
-        synced = false;
+        raw_waits(g, b.body_lo, b.body_hi);
         E.emit(OOCS_OP_H2D, s, g, blk, t);
         E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_H2D, g);
         if (g >= geo.n_ws) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_ENC, g - geo.n_ws);
@@ -244,12 +256,6 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_DEC, g);
         for (int st = 1; st <= geo.k; ++st) E.emit(OOCS_OP_STEP, s, g, blk, t, st);
         pending = g;
-        if (multi && i == nb - 1 && t + 1 < sweeps) {
-            tail(pending, -1);
-            pending = -1;
-            E.emit(OOCS_OP_EXCHANGE, s, g, blk, t);
-            synced = true;
-        }
     }
     if (pending >= 0) tail(pending, -1);  // drain epilogue
 }
@@ -334,6 +340,9 @@ static void footprint(const Geometry &geo, const oocs_op &o, std::vector<Acc> &f
             f.push_back({1, s, -1, j * MO, j * MO + b.own_hi - b.own_lo, true});
         }
         break;
+    case OOCS_OP_SEND:
+        for (int j = 0; j < 2; ++j) f.push_back({1, s, -1, j * MO, j * MO + b.own_hi - b.own_lo, false});
+        break;
     case OOCS_OP_D2H:
         for (int j = 0; j < 2; ++j) {
             if (base)
@@ -367,8 +376,7 @@ static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std
     const int N = (int)nodes.size();
     if (by_function)
         for (oocs_op &o : nodes)
-            if (o.kind != OOCS_OP_EXCHANGE)
-                o.lane = (o.kind == OOCS_OP_H2D || o.kind == OOCS_OP_CARRY) ? 0 : (o.kind == OOCS_OP_D2H ? 2 : 1);
+            o.lane = (o.kind == OOCS_OP_H2D || o.kind == OOCS_OP_CARRY) ? 0 : (o.kind == OOCS_OP_D2H ? 2 : 1);
     // 2. data-dependence edges (u < v in program order); chunks further apart than the window
     //    share no buffer (ring sizes) and meet on the host store only across one sweep
     const int L = geo.lanes, nb = geo.nb();
@@ -376,21 +384,8 @@ static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std
     std::vector<std::vector<Acc>> fp(N);
     for (int i = 0; i < N; ++i) footprint(geo, nodes[i], fp[i]);
     std::vector<std::vector<int>> pred(N), succ(N);
-    int last_barrier = -1;
     for (int v = 0; v < N; ++v) {
-        if (nodes[v].kind == OOCS_OP_EXCHANGE) {
-            for (int u = last_barrier + 1; u < v; ++u) {
-                pred[v].push_back(u);
-                succ[u].push_back(v);
-            }
-            last_barrier = v;
-            continue;
-        }
-        if (last_barrier >= 0 && nodes[last_barrier].kind == OOCS_OP_EXCHANGE) {
-            pred[v].push_back(last_barrier);
-            succ[last_barrier].push_back(v);
-        }
-        for (int u = v - 1; u > last_barrier; --u) {
+        for (int u = v - 1; u >= 0; --u) {
             if (nodes[v].g - nodes[u].g > window) break;
             if (conflict(fp[u], fp[v])) {
                 pred[v].push_back(u);
@@ -428,15 +423,6 @@ static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std
     for (int v : order) {
         const oocs_op &o = nodes[v];
         std::vector<int64_t> c(S, -1);
-        if (o.kind == OOCS_OP_EXCHANGE) {  // executed by the host after draining every stream
-            for (int u : pred[v]) {
-                for (int l = 0; l < S; ++l) c[l] = std::max(c[l], vc[u][l]);
-                c[nodes[u].lane] = std::max(c[nodes[u].lane], pos[u]);
-            }
-            vc[v] = c;
-            for (int l = 0; l < S; ++l) lane_pos[l] = std::max(lane_pos[l], c[l]);
-            continue;
-        }
         const int l = o.lane;
         if (lane_last[l] >= 0) {
             c = vc[lane_last[l]];
@@ -445,7 +431,6 @@ static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std
         std::vector<int> ps = pred[v];
         std::sort(ps.begin(), ps.end(), [&](int a, int b2) { return pos[a] > pos[b2]; });
         for (int u : ps) {
-            if (nodes[u].kind == OOCS_OP_EXCHANGE) continue;
             const int lu = nodes[u].lane;
             if (c[lu] >= pos[u]) continue;  // implied by stream order / earlier waits
             waits[v].push_back(u);

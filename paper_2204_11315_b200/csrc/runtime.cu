@@ -14,6 +14,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "oocs_internal.h"
 
 namespace oocs {
@@ -52,8 +54,20 @@ struct Plan {
     uint8_t *dvel = nullptr;         // OOCS_FLAG_RESIDENT_VELOCITY: compressed velocity kept in HBM
     bool resident_vel = false;
     float *vdec = nullptr;           // OOCS_FLAG_DECODED_VELOCITY: the rank's velocity decoded (store planes)
-    uint8_t *xbuf[4] = {};           // exchange buffers: send_lo, send_hi, recv_lo, recv_hi
-    uint64_t xbytes = 0;
+    // multi-GPU exchange region (its own cudaMalloc, so that it can be exported by CUDA IPC): four
+    // sequence flags and the ghost slots the neighbours write (oocs.h "multi-GPU")
+    uint8_t *xreg = nullptr;
+    uint64_t xreg_bytes = 0, gh_bytes = 0;  // gh_bytes = kR planes x plane_bytes (one pressure array)
+    uint32_t *xflags = nullptr;             // [READY_LO, READY_HI, FREE_LO, FREE_HI]
+    uint8_t *gh[2][2][2] = {};              // own ghost slots [side 0 = below / 1 = above][parity][pressure]
+    struct Peer {
+        uint8_t *base = nullptr;  // the neighbour's exchange region as mapped here
+        bool ipc = false;         // opened with cudaIpcOpenMemHandle (closed at destroy)
+        uint8_t *slot[2][2] = {}; // the neighbour's ghost slots this rank writes [parity][pressure]
+        uint32_t *flags = nullptr;
+    } peer[2];                              // 0 = rank-1, 1 = rank+1
+    bool connected = false;
+    int64_t seq = 0;                        // index t of the state S_t the store holds (sweeps so far)
     int *d_err = nullptr;
     cudaStream_t lanes[MAX_LANES] = {};   // copy stream of each lane (and its kernels with LANE_SINGLE_STREAM)
     cudaStream_t klanes[MAX_LANES] = {};  // kernel stream of each lane (== lanes[] with LANE_SINGLE_STREAM)
@@ -66,8 +80,6 @@ struct Plan {
     std::vector<cudaEvent_t> ev[6];  // per oocs_event_kind, rings indexed by block counter / DAG node
     int ev_ring = 0;
     cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[MAX_LANES] = {};
-    oocs_exchange_fn xfn = nullptr;
-    void *xuser = nullptr;
     bool poisoned = false;
     std::vector<KernelTiming> timing_pool;
     size_t timing_used = 0;
@@ -120,6 +132,61 @@ static inline float *vel_of(Plan *p, int set, const oocs_block &b) {
 }
 
 static cudaEvent_t evt(Plan *p, int kind, int64_t g) { return p->ev[kind][(size_t)(g % (int64_t)p->ev[kind].size())]; }
+
+// ---------------------------------------------------------------------------
+// multi-GPU exchange region: layout, stream memory operations, ghost predicates
+// ---------------------------------------------------------------------------
+enum { F_READY_LO = 0, F_READY_HI = 1, F_FREE_LO = 2, F_FREE_HI = 3 };
+// byte offset of ghost slot [side][parity][pressure] inside an exchange region (same on every rank)
+static inline uint64_t slot_off(uint64_t gh_bytes, int side, int par, int j) {
+    return 256 + (uint64_t)((side * 2 + par) * 2 + j) * al(gh_bytes);
+}
+static inline uint64_t xreg_size(uint64_t gh_bytes) { return 256 + 8 * al(gh_bytes); }
+
+// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link
+// dependency).  The wait is done by the stream's front end (no SM is held); the write is fenced, so
+// every earlier write of the stream (the ghost-slot stores) is visible before the flag.
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+static StreamValueFn stream_value_fn(const char *name) {
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint(name, &fp, cudaEnableDefault, &qr) == cudaSuccess && qr == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<StreamValueFn>(fp);
+    return nullptr;
+}
+static oocs_status wait_geq(cudaStream_t st, const uint32_t *flag, uint32_t v) {
+    static const StreamValueFn fn = stream_value_fn("cuStreamWaitValue32");
+    if (!fn) {
+        set_error("cuStreamWaitValue32 unavailable");
+        return OOCS_ERR_CUDA;
+    }
+    const int r = fn(st, (unsigned long long)(uintptr_t)flag, v, 0 /* CU_STREAM_WAIT_VALUE_GEQ (wrap-safe) */);
+    if (r) {
+        set_error("cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
+        return OOCS_ERR_CUDA;
+    }
+    return OOCS_OK;
+}
+static oocs_status write_flag(cudaStream_t st, uint32_t *flag, uint32_t v) {
+    static const StreamValueFn fn = stream_value_fn("cuStreamWriteValue32");
+    if (!fn) {
+        set_error("cuStreamWriteValue32 unavailable");
+        return OOCS_ERR_CUDA;
+    }
+    const int r = fn(st, (unsigned long long)(uintptr_t)flag, v, 0 /* CU_STREAM_WRITE_VALUE_DEFAULT: fenced */);
+    if (r) {
+        set_error("cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+        return OOCS_ERR_CUDA;
+    }
+    return OOCS_OK;
+}
+// does chunk b take its pressure planes below (above) its owned range from a ghost slot?
+static inline bool ghost_lo(const Plan *p, const oocs_block &b) {
+    return p->geo.cfg.world > 1 && p->geo.cfg.rank > 0 && &b == &p->geo.blocks[p->geo.b_lo];
+}
+static inline bool ghost_hi(const Plan *p, const oocs_block &b) {
+    return p->geo.cfg.world > 1 && p->geo.cfg.rank + 1 < p->geo.cfg.world && &b == &p->geo.blocks[p->geo.b_hi - 1];
+}
 
 static oocs_status poison(Plan *p, oocs_status st) {
     if (st == OOCS_ERR_CUDA) p->poisoned = true;
@@ -290,6 +357,9 @@ static void free_plan(Plan *p) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    for (auto &pr : p->peer)
+        if (pr.ipc && pr.base) cudaIpcCloseMemHandle(pr.base);
+    if (p->xreg) cudaFree(p->xreg);
     if (p->arena.owned && p->arena.base) cudaFree(p->arena.base);
     for (auto h : p->hstore)
         if (h) cudaFreeHost(h);
@@ -301,6 +371,7 @@ static void free_plan(Plan *p) {
 // oocs_plan_create (which then allocates exactly this) and oocs_plan_estimate (which does not).
 struct Sizes {
     size_t ws_array = 0, ws_bytes = 0, hfb = 0, staging = 0, arr_store = 0, store_bytes = 0, vdec = 0, total = 0;
+    size_t xreg = 0;  // exchange region, allocated apart from the arena (part of `total`, the device peak)
     uint64_t xbytes = 0;
     bool codec_staging = false, resident_vel = false;
 };
@@ -324,9 +395,10 @@ static Sizes compute_sizes(const Geometry &g) {
         z.vdec = (size_t)g.store_planes() * g.pstride * 4;
         z.total += al(z.vdec);
     }
-    if (g.cfg.world > 1) {
-        z.xbytes = (uint64_t)2 * g.k * R * store_pb(g);
-        z.total += 4 * al(z.xbytes);
+    if (g.cfg.world > 1) {  // the exchange region (allocated on its own for CUDA IPC; counted here)
+        z.xbytes = (uint64_t)g.k * R * store_pb(g);
+        z.xreg = al(xreg_size(z.xbytes));
+        z.total += z.xreg;
     }
     z.total += 256;  // error flag
     return z;
@@ -373,16 +445,16 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
         return OOCS_ERR_CUDA;
     }
     const Sizes z = compute_sizes(g);
-    const size_t ws_array = z.ws_array, hfb = z.hfb, arr_store = z.arr_store, total = z.total;
+    const size_t ws_array = z.ws_array, hfb = z.hfb, arr_store = z.arr_store, total = z.total - z.xreg;
     const bool codec_staging = z.codec_staging;
     p->ws_bytes = z.ws_bytes;
     p->staging_bytes = z.staging;
     p->store_bytes = z.store_bytes;
     p->resident_vel = z.resident_vel;
-    p->xbytes = z.xbytes;
-    p->arena_bytes = total;
-    if (g.cfg.device_capacity && total > g.cfg.device_capacity) {
-        set_error("device arena (" + std::to_string(total) + " B) exceeds device_capacity");
+    p->gh_bytes = z.xbytes;
+    p->arena_bytes = z.total;
+    if (g.cfg.device_capacity && z.total > g.cfg.device_capacity) {
+        set_error("device arena (" + std::to_string(z.total) + " B) exceeds device_capacity");
         delete p;
         return OOCS_ERR_DEVICE_OOM;
     }
@@ -427,8 +499,6 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
     }
     if (p->resident_vel) p->dvel = (uint8_t *)p->arena.take(arr_store);
     if (z.vdec) p->vdec = (float *)p->arena.take(z.vdec);
-    if (g.cfg.world > 1)
-        for (int i = 0; i < 4; ++i) p->xbuf[i] = (uint8_t *)p->arena.take(p->xbytes);
     p->d_err = (int *)p->arena.take(sizeof(int));
     if (!p->d_err) {
         set_error("internal: arena carve-out overflow");
@@ -436,10 +506,25 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
         return OOCS_ERR_STATE;
     }
     // zero the working sets so halo columns / padding are defined
-    if (cudaMemset(p->arena.base, 0, total) != cudaSuccess) {
+    if (cudaMemset(p->arena.base, 0, p->arena.used) != cudaSuccess) {
         set_error("cudaMemset of the arena failed");
         free_plan(p);
         return OOCS_ERR_CUDA;
+    }
+    if (g.cfg.world > 1) {
+        p->xreg_bytes = xreg_size(p->gh_bytes);
+        ce = cudaMalloc((void **)&p->xreg, p->xreg_bytes);
+        if (ce != cudaSuccess || cudaMemset(p->xreg, 0, p->xreg_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            p->xreg = ce == cudaSuccess ? p->xreg : nullptr;
+            set_error("allocation of the multi-GPU exchange region failed");
+            free_plan(p);
+            return OOCS_ERR_DEVICE_OOM;
+        }
+        p->xflags = reinterpret_cast<uint32_t *>(p->xreg);
+        for (int side = 0; side < 2; ++side)
+            for (int par = 0; par < 2; ++par)
+                for (int j = 0; j < 2; ++j) p->gh[side][par][j] = p->xreg + slot_off(p->gh_bytes, side, par, j);
     }
     if (g.host_store) {
         for (int a = 0; a < N_ARRAYS; ++a) {
@@ -506,59 +591,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
 // STEP s updates array (s odd ? 1 : 2) from the other one (leapfrog in place).
 static inline int upd_array(int s) { return (s & 1) ? 1 : 2; }
 
-static oocs_status do_exchange(Plan *p, int64_t sweep, oocs_stats *stats) {
-    const Geometry &g = p->geo;
-    const int64_t kR = (int64_t)g.k * R;
-    const int64_t Zlo = g.blocks[g.b_lo].own_lo, Zhi = g.blocks[g.b_hi - 1].own_hi;
-    const bool has_lo = g.cfg.rank > 0, has_hi = g.cfg.rank + 1 < g.cfg.world;
-    for (int l = 0; l < g.lanes; ++l) {
-        CU(cudaStreamSynchronize(p->lanes[l]));
-        CU(cudaStreamSynchronize(p->klanes[l]));
-    }
-    for (int c = 0; c < 3; ++c) CU(cudaStreamSynchronize(p->cstream[c]));
-    cudaStream_t st = p->lanes[0];
-    const uint64_t arr = (uint64_t)kR * spb(p);
-    // pack: planes [Zlo, Zlo+kR) -> send_lo ; [Zhi-kR, Zhi) -> send_hi ; arrays 1, 2
-    for (int a = 1; a <= 2; ++a) {
-        const uint64_t o = (uint64_t)(a - 1) * arr;
-        if (g.host_store) {
-            if (has_lo) CU(cudaMemcpyAsync(p->xbuf[0] + o, p->hstore[a] + hoff(p, Zlo), arr, cudaMemcpyHostToDevice, st));
-            if (has_hi) CU(cudaMemcpyAsync(p->xbuf[1] + o, p->hstore[a] + hoff(p, Zhi - kR), arr, cudaMemcpyHostToDevice, st));
-        } else {
-            uint8_t *S = p->dstore[p->cur ^ 1][a];
-            if (has_lo) CU(cudaMemcpyAsync(p->xbuf[0] + o, S + hoff(p, Zlo), arr, cudaMemcpyDeviceToDevice, st));
-            if (has_hi) CU(cudaMemcpyAsync(p->xbuf[1] + o, S + hoff(p, Zhi - kR), arr, cudaMemcpyDeviceToDevice, st));
-        }
-    }
-    CU(cudaStreamSynchronize(st));
-    if (!p->xfn) {
-        set_error("world > 1 but no exchange callback installed (oocs_set_exchange)");
-        return OOCS_ERR_EXCHANGE;
-    }
-    const int rc = p->xfn(p->xuser, sweep, has_lo ? p->xbuf[0] : nullptr, has_hi ? p->xbuf[1] : nullptr,
-                          has_lo ? p->xbuf[2] : nullptr, has_hi ? p->xbuf[3] : nullptr, p->xbytes, (void *)st);
-    if (rc) {
-        set_error("halo exchange callback failed");
-        return OOCS_ERR_EXCHANGE;
-    }
-    // unpack: recv_lo -> ghost planes [Zlo-kR, Zlo) ; recv_hi -> [Zhi, Zhi+kR)
-    for (int a = 1; a <= 2; ++a) {
-        const uint64_t o = (uint64_t)(a - 1) * arr;
-        if (g.host_store) {
-            if (has_lo) CU(cudaMemcpyAsync(p->hstore[a] + hoff(p, Zlo - kR), p->xbuf[2] + o, arr, cudaMemcpyDeviceToHost, st));
-            if (has_hi) CU(cudaMemcpyAsync(p->hstore[a] + hoff(p, Zhi), p->xbuf[3] + o, arr, cudaMemcpyDeviceToHost, st));
-        } else {
-            uint8_t *S = p->dstore[p->cur ^ 1][a];
-            if (has_lo) CU(cudaMemcpyAsync(S + hoff(p, Zlo - kR), p->xbuf[2] + o, arr, cudaMemcpyDeviceToDevice, st));
-            if (has_hi) CU(cudaMemcpyAsync(S + hoff(p, Zhi), p->xbuf[3] + o, arr, cudaMemcpyDeviceToDevice, st));
-        }
-    }
-    CU(cudaStreamSynchronize(st));
-    if (stats) stats->bytes_exchange += (uint64_t)(has_lo + has_hi) * p->xbytes;
-    return OOCS_OK;
-}
-
-// Issue one work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, EXCHANGE) on stream st.  The device
+// Issue one work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, SEND) on stream st.  The device
 // store's read/write buffers follow from the op's sweep: S_t = dstore[cur0 ^ (sweep & 1)].
 static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cur0, oocs_stats *stats) {
     const Geometry &g = p->geo;
@@ -581,12 +614,20 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
             for (int a = 0; a < N_ARRAYS; ++a)
                 CU(copy_1d(wsa(p, w, a) + off * g.pstride, p->hstore[a] + hoff(p, b.body_lo), nplanes * spb(p),
                            cudaMemcpyHostToDevice, st, p->copy_chunk));
+            if (stats) stats->bytes_h2d += (uint64_t)N_ARRAYS * nplanes * spb(p);
         } else {
-            for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
-                CU(copy_1d(p->hf[s] + ((uint64_t)a * g.max_ext + off) * PB, p->hstore[a] + hoff(p, b.body_lo),
-                           nplanes * PB, cudaMemcpyHostToDevice, st, p->copy_chunk));
+            // multi-GPU edge chunks: the pressure planes beyond the slab come from the ghost slots
+            // (written by the neighbour over NVLink), never from the host store
+            const int64_t plo = ghost_lo(p, b) ? std::max(b.body_lo, b.own_lo) : b.body_lo;
+            const int64_t phi = ghost_hi(p, b) ? std::min(b.body_hi, b.own_hi) : b.body_hi;
+            for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a) {
+                const int64_t lo = a ? plo : b.body_lo, hi = a ? phi : b.body_hi;
+                if (hi <= lo) continue;
+                CU(copy_1d(p->hf[s] + ((uint64_t)a * g.max_ext + (lo - b.ext_lo)) * PB, p->hstore[a] + hoff(p, lo),
+                           (hi - lo) * PB, cudaMemcpyHostToDevice, st, p->copy_chunk));
+                if (stats) stats->bytes_h2d += (uint64_t)(hi - lo) * PB;
+            }
         }
-        if (stats) stats->bytes_h2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * spb(p);
         break;
     }
     case OOCS_OP_CARRY: {
@@ -612,21 +653,54 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         break;
     }
     case OOCS_OP_DECODE: {
-        const void *src[N_ARRAYS];
-        float *dst[N_ARRAYS];
-        for (int a = 0; a < N_ARRAYS; ++a) {
-            if (a == 0 && p->resident_vel)
-                src[a] = p->dvel + hoff(p, b.ext_lo);
-            else if (g.host_store)
-                src[a] = p->hf[s] + (uint64_t)a * g.max_ext * PB;
-            else
-                src[a] = p->dstore[p->cur][a] + hoff(p, b.ext_lo);
-            dst[a] = wsa(p, w, a);
-        }
+        // compressed source of interior plane z of array a for this chunk
+        auto src_of = [&](int a, int64_t z) -> const void * {
+            if (a == 0 && p->resident_vel) return p->dvel + hoff(p, z);
+            if (g.host_store) return p->hf[s] + ((uint64_t)a * g.max_ext + (z - b.ext_lo)) * PB;
+            return p->dstore[p->cur][a] + hoff(p, z);
+        };
         // with the velocity kept decoded only the two pressures are decoded
         const int a0 = p->vdec ? 1 : 0;
-        oocs_status r = k_decode(p, src + a0, dst + a0, N_ARRAYS - a0, E, st, stats);
-        if (r) return r;
+        const bool glo = ghost_lo(p, b), ghi = ghost_hi(p, b);
+        if (!glo && !ghi) {
+            const void *src[N_ARRAYS];
+            float *dst[N_ARRAYS];
+            for (int a = 0; a < N_ARRAYS; ++a) {
+                src[a] = src_of(a, b.ext_lo);
+                dst[a] = wsa(p, w, a);
+            }
+            oocs_status r = k_decode(p, src + a0, dst + a0, N_ARRAYS - a0, E, st, stats);
+            if (r) return r;
+            break;
+        }
+        // multi-GPU edge chunk: the pressure planes beyond the slab are decoded straight out of the ghost
+        // slots of state S_t, once the neighbour has written them (READY >= t); the neighbour's FREE flag
+        // then releases the slot for S_{t+2}
+        const uint32_t t_idx = (uint32_t)(p->seq + o.sweep);
+        const int par = (int)(t_idx & 1u);
+        const int64_t kR = (int64_t)g.k * R, mlo = glo ? b.own_lo : b.ext_lo, mhi = ghi ? b.own_hi : b.ext_hi;
+        if (a0 == 0) {
+            oocs_status r = k_decode(p, src_of(0, b.ext_lo), wsa(p, w, 0), E, st, stats);
+            if (r) return r;
+        }
+        {
+            const void *src[2] = {src_of(1, mlo), src_of(2, mlo)};
+            float *dst[2] = {wsa(p, w, 1) + (mlo - b.ext_lo) * g.pstride, wsa(p, w, 2) + (mlo - b.ext_lo) * g.pstride};
+            oocs_status r = k_decode(p, src, dst, 2, mhi - mlo, st, stats);
+            if (r) return r;
+        }
+        for (int side = 0; side < 2; ++side) {
+            if (!(side ? ghi : glo)) continue;
+            if (oocs_status r = wait_geq(st, &p->xflags[side ? F_READY_HI : F_READY_LO], t_idx)) return r;
+            const int64_t z0 = side ? b.own_hi : b.ext_lo;
+            const void *src[2] = {p->gh[side][par][0], p->gh[side][par][1]};
+            float *dst[2] = {wsa(p, w, 1) + (z0 - b.ext_lo) * g.pstride, wsa(p, w, 2) + (z0 - b.ext_lo) * g.pstride};
+            oocs_status r = k_decode(p, src, dst, 2, kR, st, stats);
+            if (r) return r;
+            // the lower neighbour's upper sends / the upper neighbour's lower sends are consumed up to S_t
+            Plan::Peer &pr = p->peer[side];
+            if (oocs_status r2 = write_flag(st, pr.flags + (side ? F_FREE_LO : F_FREE_HI), t_idx + 1)) return r2;
+        }
         break;
     }
     case OOCS_OP_STEP: {
@@ -687,10 +761,28 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         if (stats) stats->bytes_d2h += (uint64_t)2 * W * spb(p);
         break;
     }
-    case OOCS_OP_EXCHANGE: {
-        oocs_status r = do_exchange(p, o.sweep, stats);
-        if (r) return r;
-        if (!g.host_store) p->cur ^= 1;
+    case OOCS_OP_SEND: {
+        // multi-GPU: this edge chunk's first (arg bit 0) / last (bit 1) kR encoded planes of S_{t+1},
+        // straight from the encode output into the neighbour's ghost slot over NVLink (peer stores from
+        // a copy kernel on this stream), then the neighbour's READY flag.  The slot of parity (t+1)&1
+        // last held S_{t-1}: wait until the neighbour has consumed it (our FREE flag >= t).
+        const uint32_t t1 = (uint32_t)(p->seq + o.sweep + 1);
+        const int par = (int)(t1 & 1u);
+        const int64_t kR = (int64_t)g.k * R, W = b.own_hi - b.own_lo;
+        auto enc_out = [&](int j, int64_t plane_off) -> const uint8_t * {
+            if (g.host_store) return p->hf[s] + ((uint64_t)j * g.max_own + plane_off) * PB;
+            return p->dstore[p->cur ^ 1][1 + j] + hoff(p, b.own_lo + plane_off);
+        };
+        for (int side = 0; side < 2; ++side) {
+            if (!((o.arg >> side) & 1)) continue;
+            Plan::Peer &pr = p->peer[side];
+            if (t1 >= 2)
+                if (oocs_status r = wait_geq(st, &p->xflags[side ? F_FREE_HI : F_FREE_LO], t1 - 1)) return r;
+            const int64_t off = side ? W - kR : 0;
+            CU(launch_peer_copy(enc_out(0, off), pr.slot[par][0], enc_out(1, off), pr.slot[par][1], p->gh_bytes, st));
+            if (oocs_status r = write_flag(st, pr.flags + (side ? F_READY_LO : F_READY_HI), t1)) return r;
+            if (stats) stats->bytes_exchange += 2 * p->gh_bytes;
+        }
         break;
     }
     default:
@@ -700,7 +792,10 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
     return OOCS_OK;
 }
 
-static bool is_kernel_op(int k) { return k == OOCS_OP_DECODE || k == OOCS_OP_STEP || k == OOCS_OP_ENCODE; }
+// SEND is a kernel-stream op too: a peer copy kernel plus stream memory operations
+static bool is_kernel_op(int k) {
+    return k == OOCS_OP_DECODE || k == OOCS_OP_STEP || k == OOCS_OP_ENCODE || k == OOCS_OP_SEND;
+}
 static bool is_work_op(int k) { return k != OOCS_OP_WAIT && k != OOCS_OP_RECORD; }
 
 // OOCS_FLAG_TIMELINE: event pair around a work op
@@ -738,7 +833,7 @@ static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int
     const bool tl = g.cfg.flags & OOCS_FLAG_TIMELINE;
     // a WAIT goes to the stream of the lane's next work op, a RECORD to the stream of its previous one
     auto work_stream = [&](const oocs_op &o) {
-        return o.kind == OOCS_OP_EXCHANGE ? p->lanes[0] : is_kernel_op(o.kind) ? p->klanes[o.lane] : p->lanes[o.lane];
+        return is_kernel_op(o.kind) ? p->klanes[o.lane] : p->lanes[o.lane];
     };
     std::vector<cudaStream_t> op_stream(ops.size());
     {
@@ -766,7 +861,7 @@ static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int
             CU(cudaEventRecord(evt(p, o.arg, o.ev_g), st));
             continue;
         }
-        if (o.kind != OOCS_OP_EXCHANGE) {
+        {
             // program order within the lane across its two streams
             cudaStream_t &lw = last_work[o.lane];
             if (lw && lw != st) {
@@ -782,9 +877,23 @@ static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int
         }
         oocs_status r = issue_work(p, o, st, cur0, stats);
         if (r) return r;
-        if (tl) CU(cudaEventRecord(p->span_events[sp].second, o.kind == OOCS_OP_EXCHANGE ? p->lanes[0] : st));
+        if (tl) CU(cudaEventRecord(p->span_events[sp].second, st));
     }
     return OOCS_OK;
+}
+
+// Watchdog: a run that makes no progress for OOCS_WATCHDOG_S seconds (default 600; 0 disables) is
+// aborted -- in a multi-GPU job that means a neighbour stopped writing its flags.
+static bool stalled_ok(Plan *p, std::chrono::steady_clock::time_point since) {
+    static const double limit = [] {
+        const char *e = std::getenv("OOCS_WATCHDOG_S");
+        return e ? std::strtod(e, nullptr) : 600.0;
+    }();
+    if (limit <= 0) return true;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - since).count() < limit) return true;
+    set_error("no progress for " + std::to_string((int)limit) + " s (a multi-GPU neighbour stopped?); plan poisoned");
+    p->poisoned = true;
+    return false;
 }
 
 // Executor 2 (default): a host dispatcher over the schedule's dependency graph.  Every WAIT of the
@@ -822,13 +931,8 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
                 const int64_t pr = key(o.arg, o.ev_g);
                 if (pr >= 0) lane_waits[o.lane].push_back(pr);
             } else {
-                if (o.kind == OOCS_OP_EXCHANGE) {
-                    for (size_t j = 0; j < i; ++j)  // a host-synchronous barrier over everything before it
-                        if (is_work_op(ops[j].kind)) deps.push_back((int64_t)j);
-                } else {
-                    if (last_work[o.lane] >= 0) deps.push_back(last_work[o.lane]);
-                    for (int64_t d : lane_waits[o.lane]) deps.push_back(d);
-                }
+                if (last_work[o.lane] >= 0) deps.push_back(last_work[o.lane]);
+                for (int64_t d : lane_waits[o.lane]) deps.push_back(d);
                 lane_waits[o.lane].clear();
                 last_work[o.lane] = (int64_t)i;
             }
@@ -849,7 +953,6 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
         case OOCS_OP_H2D: return p->cstream[0];
         case OOCS_OP_D2H: return p->cstream[1];
         case OOCS_OP_CARRY: return p->cstream[2];
-        case OOCS_OP_EXCHANGE: return p->lanes[0];
         default: return p->klanes[o.lane];
         }
     };
@@ -857,6 +960,8 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
     std::vector<cudaStream_t> where(n, nullptr);
     for (size_t i = 0; i < n; ++i)
         if (!is_work_op(ops[i].kind)) issued[i] = done[i] = 1;
+    // a query error other than NotReady is a sticky device fault: stop and poison the plan
+    cudaError_t qerr = cudaSuccess;
     auto complete = [&](int64_t d) -> bool {
         if (done[d]) return true;
         const cudaError_t e = cudaEventQuery(p->op_done[d]);
@@ -864,33 +969,37 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
             done[d] = 1;
             return true;
         }
-        if (e != cudaErrorNotReady) (void)cudaGetLastError();
+        if (e != cudaErrorNotReady) {
+            qerr = e;
+            (void)cudaGetLastError();
+        }
         return false;
     };
     size_t first = 0;
+    auto last_progress = std::chrono::steady_clock::now();
     while (first < n) {
+        if (qerr != cudaSuccess) {
+            set_error(std::string("device fault while executing the schedule: ") + cudaGetErrorString(qerr));
+            return OOCS_ERR_CUDA;
+        }
+        if (!stalled_ok(p, last_progress)) return OOCS_ERR_EXCHANGE;
         bool progress = false;
         for (size_t i = first; i < n; ++i) {
             if (issued[i]) continue;
             const oocs_op &o = ops[i];
-            const bool copy = !is_kernel_op(o.kind) && o.kind != OOCS_OP_EXCHANGE;
+            const bool copy = !is_kernel_op(o.kind);
             bool ready = true;
             for (int64_t k = dep_start[i]; k < dep_start[i + 1] && ready; ++k) {
                 const int64_t d = deps[k];
-                ready = issued[d] && (!(copy || o.kind == OOCS_OP_EXCHANGE) || complete(d));
+                ready = issued[d] && (!copy || complete(d));
             }
-            if (!ready) {
-                if (o.kind == OOCS_OP_EXCHANGE) break;  // a barrier: nothing after it may pass
-                continue;
-            }
+            if (!ready) continue;
             cudaStream_t st = stream_of(o);
-            if (!copy && o.kind != OOCS_OP_EXCHANGE)
+            if (!copy)
                 for (int64_t k = dep_start[i]; k < dep_start[i + 1]; ++k) {
                     const int64_t d = deps[k];
                     if (where[d] != st && !done[d]) CU(cudaStreamWaitEvent(st, p->op_done[d], 0));
                 }
-            if (o.kind == OOCS_OP_EXCHANGE)
-                for (int c = 0; c < 3; ++c) CU(cudaStreamSynchronize(p->cstream[c]));
             size_t sp = 0;
             if (tl) {
                 oocs_status r = span_begin(p, o, st, &sp);
@@ -905,7 +1014,8 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
             progress = true;
         }
         while (first < n && issued[first]) ++first;
-        if (!progress) std::this_thread::yield();
+        if (progress) last_progress = std::chrono::steady_clock::now();
+        else std::this_thread::yield();
     }
     return OOCS_OK;
 }
@@ -929,9 +1039,9 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
         set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
         return OOCS_ERR_CONFIG;
     }
-    if (g.cfg.world > 1 && !p->xfn) {
-        set_error("world > 1 requires oocs_set_exchange");
-        return OOCS_ERR_STATE;
+    if (g.cfg.world > 1 && !p->connected) {
+        set_error("world > 1: connect the neighbours first (oocs_peer_handle / oocs_peer_connect)");
+        return OOCS_ERR_EXCHANGE;
     }
     CU(cudaSetDevice(g.cfg.device));
     oocs_stats stats;
@@ -963,7 +1073,18 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
         CU(cudaStreamWaitEvent(p->lanes[0], p->cdone[c], 0));
     }
     CU(cudaEventRecord(p->t1, p->lanes[0]));
-    CU(cudaEventSynchronize(p->t1));
+    {
+        // poll instead of blocking: a multi-GPU neighbour that never writes its flag must not hang the
+        // process (the watchdog turns it into OOCS_ERR_EXCHANGE and a poisoned plan)
+        const auto t_start = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t e = cudaEventQuery(p->t1);
+            if (e == cudaSuccess) break;
+            if (e != cudaErrorNotReady) CU(e);
+            if (!stalled_ok(p, t_start)) return poison(p, OOCS_ERR_EXCHANGE);
+            std::this_thread::sleep_for(std::chrono::microseconds(g.cfg.world > 1 ? 20 : 200));
+        }
+    }
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, p->t0, p->t1));
     stats.wall_ms = ms;
@@ -985,7 +1106,7 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
         for (const oocs_span &s : p->spans) {
             const int e = s.kind == OOCS_OP_H2D ? 0 : s.kind == OOCS_OP_D2H ? 1
                         : (s.kind == OOCS_OP_DECODE || s.kind == OOCS_OP_STEP || s.kind == OOCS_OP_ENCODE) ? 2
-                        : s.kind == OOCS_OP_EXCHANGE ? 3 : -1;
+                        : s.kind == OOCS_OP_SEND ? 3 : -1;
             if (e >= 0) iv[e].emplace_back(s.start_ms, s.end_ms);
         }
         for (int e = 0; e < 4; ++e) {
@@ -1004,6 +1125,7 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
             stats.busy_ms[e] = tot;
         }
     }
+    p->seq += steps / g.k;  // the store now holds S_{seq}
     int herr = 0;
     CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     stats.data_error = herr;
@@ -1034,7 +1156,33 @@ static oocs_status check_range(const Plan *p, int32_t array, int64_t a_lo, int64
     return OOCS_OK;
 }
 
-static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
+// Multi-GPU: the pressure ghost planes of a rank's store are a mirror of its ghost slots (the slots are
+// what the pipeline reads and the neighbours write).  After a write into the store (load, write_raw) the
+// ghost planes go to the slots of the current state; before a read they come back from them.
+static oocs_status sync_ghosts(Plan *p, int32_t array, int64_t a_lo, int64_t a_hi, bool to_slots) {
+    const Geometry &g = p->geo;
+    if (g.cfg.world == 1 || array == 0) return OOCS_OK;
+    const int64_t kR = (int64_t)g.k * R;
+    const int par = (int)(p->seq & 1);
+    for (int side = 0; side < 2; ++side) {
+        if (side == 0 && g.cfg.rank == 0) continue;
+        if (side == 1 && g.cfg.rank + 1 == g.cfg.world) continue;
+        const int64_t z0 = side ? g.store_hi - kR : g.store_lo;  // interior planes of the ghost range
+        if (a_hi <= z0 + R || z0 + kR + R <= a_lo) continue;
+        uint8_t *slot = p->gh[side][par][array - 1];
+        if (g.host_store) {
+            uint8_t *h = p->hstore[array] + hoff(p, z0);
+            if (to_slots) CU(cudaMemcpy(slot, h, p->gh_bytes, cudaMemcpyHostToDevice));
+            else CU(cudaMemcpy(h, slot, p->gh_bytes, cudaMemcpyDeviceToHost));
+        } else {
+            uint8_t *d = p->dstore[p->cur][array] + hoff(p, z0);
+            CU(cudaMemcpy(to_slots ? slot : d, to_slots ? d : slot, p->gh_bytes, cudaMemcpyDeviceToDevice));
+        }
+    }
+    return OOCS_OK;
+}
+
+static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, int64_t a_hi, bool dev_src) {
     oocs_status st = check_range(p, array, a_lo, a_hi);
     if (st) return st;
     const Geometry &g = p->geo;
@@ -1047,7 +1195,8 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
     uint8_t *stage = reinterpret_cast<uint8_t *>(p->ws[0][1]);
     for (int64_t a = a_lo; a < a_hi; a += chunk) {
         const int64_t n = std::min(chunk, a_hi - a);
-        CU(copy_raw_to_ws(ws, src + (a - a_lo) * g.ax * g.ay, g, n, cudaMemcpyHostToDevice, s));
+        CU(copy_raw_to_ws(ws, src + (a - a_lo) * g.ax * g.ay, g, n,
+                          dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         const int64_t z = a - R;
         if (pitched_store(g)) {  // BASELINE: the store holds working-buffer rows
             CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), ws, n * spb(p), cudaMemcpyDeviceToHost, s));
@@ -1070,6 +1219,7 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
         }
         CU(cudaStreamSynchronize(s));
     }
+    if (oocs_status r = sync_ghosts(p, array, a_lo, a_hi, true)) return r;
     int herr = 0;
     CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (herr) {
@@ -1079,11 +1229,12 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
     return OOCS_OK;
 }
 
-static oocs_status store(Plan *p, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
+static oocs_status store(Plan *p, int32_t array, float *dst, int64_t a_lo, int64_t a_hi, bool dev_dst) {
     oocs_status st = check_range(p, array, a_lo, a_hi);
     if (st) return st;
     const Geometry &g = p->geo;
     CU(cudaSetDevice(g.cfg.device));
+    if (oocs_status r = sync_ghosts(p, array, a_lo, a_hi, false)) return r;
     cudaStream_t s = p->lanes[0];
     const int64_t chunk = g.max_ext / 4 * 4;
     float *ws = p->ws[0][0];
@@ -1104,7 +1255,8 @@ static oocs_status store(Plan *p, int32_t array, float *dst, int64_t a_lo, int64
             oocs_status r = k_decode(p, src, ws, n, s, nullptr);
             if (r) return r;
         }
-        CU(copy_ws_to_raw(dst + (a - a_lo) * g.ax * g.ay, ws, g, n, cudaMemcpyDeviceToHost, s));
+        CU(copy_ws_to_raw(dst + (a - a_lo) * g.ax * g.ay, ws, g, n,
+                          dev_dst ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
     }
     return OOCS_OK;
@@ -1115,6 +1267,8 @@ static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int6
     if (st) return st;
     const Geometry &g = p->geo;
     CU(cudaSetDevice(g.cfg.device));
+    if (!write)
+        if (oocs_status r = sync_ghosts(p, array, a_lo, a_hi, false)) return r;
     const uint64_t off = hoff(p, a_lo - R), n = (uint64_t)(a_hi - a_lo) * pb(p);
     if (pitched_store(g)) {  // raw bytes are the identity codec's planes (rows of ax floats)
         const int64_t rows = (a_hi - a_lo) * g.ay;
@@ -1157,6 +1311,18 @@ static oocs_status raw_io(Plan *p, int32_t array, void *host, int64_t a_lo, int6
 // C ABI
 // ===========================================================================
 using namespace oocs;
+
+// the exchange-region handle oocs_peer_handle exports (OOCS_PEER_HANDLE_BYTES)
+constexpr uint64_t PEER_MAGIC = 0x5245455053434f4fULL;  // "OOCSPEER"
+struct PeerBlob {
+    uint64_t magic;
+    uint32_t version, pid;
+    int32_t device, rank, world, k, codec, pad;
+    int64_t nx, ny, nz, plane_bytes;
+    uint64_t gh_bytes, xreg_bytes, dev_ptr;
+    cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(PeerBlob) <= OOCS_PEER_HANDLE_BYTES, "peer handle blob too large");
 
 static oocs_status guard(const oocs_plan *p) {
     if (!p) {
@@ -1216,10 +1382,111 @@ oocs_status oocs_plan_estimate(const oocs_config *cfg, oocs_plan_info *info) {
     return OOCS_OK;
 }
 
-oocs_status oocs_set_exchange(oocs_plan *plan, oocs_exchange_fn fn, void *user) {
+oocs_status oocs_peer_handle(const oocs_plan *plan, void *out) {
     if (oocs_status st = guard(plan)) return st;
-    plan->xfn = fn;
-    plan->xuser = user;
+    if (!out) {
+        set_error("oocs_peer_handle: out is NULL");
+        return OOCS_ERR_CONFIG;
+    }
+    if (!plan->xreg) {
+        set_error("oocs_peer_handle: world == 1, the plan has no exchange region");
+        return OOCS_ERR_STATE;
+    }
+    const Geometry &g = plan->geo;
+    CU(cudaSetDevice(g.cfg.device));
+    PeerBlob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = PEER_MAGIC;
+    b.version = OOCS_ABI_VERSION;
+    b.pid = (uint32_t)getpid();
+    b.device = g.cfg.device;
+    b.rank = g.cfg.rank;
+    b.world = g.cfg.world;
+    b.k = g.k;
+    b.nx = g.nx;
+    b.ny = g.ny;
+    b.nz = g.nz;
+    b.plane_bytes = g.plane_bytes;
+    b.gh_bytes = plan->gh_bytes;
+    b.xreg_bytes = plan->xreg_bytes;
+    b.dev_ptr = (uint64_t)(uintptr_t)plan->xreg;
+    b.codec = g.codec;
+    CU(cudaIpcGetMemHandle(&b.ipc, plan->xreg));
+    std::memset(out, 0, OOCS_PEER_HANDLE_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+    return OOCS_OK;
+}
+
+oocs_status oocs_peer_connect(oocs_plan *plan, const void *lower, const void *upper) {
+    if (oocs_status st = guard(plan)) return st;
+    const Geometry &g = plan->geo;
+    if (!plan->xreg) {
+        set_error("oocs_peer_connect: world == 1, nothing to connect");
+        return OOCS_ERR_STATE;
+    }
+    const void *blob[2] = {lower, upper};
+    const bool need[2] = {g.cfg.rank > 0, g.cfg.rank + 1 < g.cfg.world};
+    PeerBlob pb2[2];
+    for (int side = 0; side < 2; ++side) {
+        if (!need[side]) continue;
+        if (!blob[side]) {
+            set_error(side ? "oocs_peer_connect: upper (rank+1) handle missing" : "oocs_peer_connect: lower (rank-1) handle missing");
+            return OOCS_ERR_CONFIG;
+        }
+        std::memcpy(&pb2[side], blob[side], sizeof(PeerBlob));
+        const PeerBlob &b = pb2[side];
+        if (b.magic != PEER_MAGIC || b.version != OOCS_ABI_VERSION || b.world != g.cfg.world ||
+            b.rank != g.cfg.rank + (side ? 1 : -1) || b.k != g.k || b.nx != g.nx || b.ny != g.ny || b.nz != g.nz ||
+            b.plane_bytes != g.plane_bytes || b.codec != g.codec || b.gh_bytes != plan->gh_bytes ||
+            b.xreg_bytes != plan->xreg_bytes) {
+            set_error("oocs_peer_connect: the handle is not the neighbour's of the same job geometry");
+            return OOCS_ERR_CONFIG;
+        }
+    }
+    CU(cudaSetDevice(g.cfg.device));
+    for (auto &pr : plan->peer) {  // re-connect: drop the previous mappings
+        if (pr.ipc && pr.base) cudaIpcCloseMemHandle(pr.base);
+        pr = Plan::Peer{};
+    }
+    plan->connected = false;
+    for (int side = 0; side < 2; ++side) {
+        if (!need[side]) continue;
+        const PeerBlob &b = pb2[side];
+        Plan::Peer &pr = plan->peer[side];
+        if (b.pid == (uint32_t)getpid()) {  // same process: the pointer itself
+            if (b.device == g.cfg.device) {
+                // one context would hold both ranks' streams: a rank's flag wait at the head of a hardware
+                // queue could block the neighbour's producing work queued behind it (false dependency)
+                set_error("oocs_peer_connect: ranks sharing one device must be separate processes");
+                return OOCS_ERR_CONFIG;
+            }
+            pr.base = reinterpret_cast<uint8_t *>((uintptr_t)b.dev_ptr);
+            if (b.device != g.cfg.device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    cudaGetLastError();
+                    set_error(std::string("oocs_peer_connect: peer access failed: ") + cudaGetErrorString(e));
+                    return OOCS_ERR_EXCHANGE;
+                }
+                cudaGetLastError();
+            }
+        } else {
+            void *ptr = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                set_error(std::string("oocs_peer_connect: cudaIpcOpenMemHandle failed: ") + cudaGetErrorString(e));
+                return OOCS_ERR_EXCHANGE;
+            }
+            pr.base = static_cast<uint8_t *>(ptr);
+            pr.ipc = true;
+        }
+        // we write the lower neighbour's upper slots and the upper neighbour's lower slots
+        for (int par = 0; par < 2; ++par)
+            for (int j = 0; j < 2; ++j) pr.slot[par][j] = pr.base + slot_off(plan->gh_bytes, 1 - side, par, j);
+        pr.flags = reinterpret_cast<uint32_t *>(pr.base);
+    }
+    plan->connected = true;
     return OOCS_OK;
 }
 
@@ -1230,12 +1497,22 @@ oocs_status oocs_destroy(oocs_plan *plan) {
 
 oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
-    return poison(plan, load(plan, array, src, a_lo, a_hi));
+    return poison(plan, load(plan, array, src, a_lo, a_hi, false));
+}
+
+oocs_status oocs_load_device(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, load(plan, array, src, a_lo, a_hi, true));
 }
 
 oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
-    return poison(plan, store(plan, array, dst, a_lo, a_hi));
+    return poison(plan, store(plan, array, dst, a_lo, a_hi, false));
+}
+
+oocs_status oocs_store_device(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, store(plan, array, dst, a_lo, a_hi, true));
 }
 
 oocs_status oocs_store_read_raw(oocs_plan *plan, int32_t array, void *dst, int64_t a_lo, int64_t a_hi) {

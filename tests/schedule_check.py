@@ -1,7 +1,7 @@
 """Structural race checker for lowered pipeline schedules (test tooling; SPEC validate_exclusive S:L409-417).
 
 Builds the happens-before relation of an op list (lane FIFO order, RECORD -> WAIT
-event edges, EXCHANGE = full barrier) and the memory footprint of every op
+event edges) and the memory footprint of every op
 (buffer, array, plane range, read/write), then reports every pair of ops that
 touch overlapping memory with at least one write but are not ordered.
 """
@@ -83,6 +83,9 @@ def footprint(op, blocks, geo):
         for j in range(2):
             out.append((("hf", s), j * MO, j * MO + own_hi - own_lo, False))
             out.append((("host", 1 + j), own_lo, own_hi, True))
+    elif kind == "SEND":  # multi-GPU: reads edge planes of the encoded output (peer side: device flags)
+        for j in range(2):
+            out.append((("hf", s), j * MO, j * MO + own_hi - own_lo, False))
     return out
 
 
@@ -93,11 +96,6 @@ def happens_before(ops):
     last_on_lane = {}
     last_record = {}
     for i, op in enumerate(ops):
-        if op["kind"] == "EXCHANGE":
-            for j in range(i):
-                succ[j].add(i)
-            last_on_lane = {l: i for l in range(8)}
-            continue
         l = op["lane"]
         if l in last_on_lane:
             succ[last_on_lane[l]].add(i)
@@ -119,7 +117,7 @@ def happens_before(ops):
 
 def violations(ops, blocks, geo, limit=50):
     reach = happens_before(ops)
-    fps = [footprint(op, blocks, geo) if op["kind"] not in ("WAIT", "RECORD", "EXCHANGE") else [] for op in ops]
+    fps = [footprint(op, blocks, geo) if op["kind"] not in ("WAIT", "RECORD") else [] for op in ops]
     bad = []
     idx = [i for i, f in enumerate(fps) if f]
     for ii, i in enumerate(idx):

@@ -42,6 +42,7 @@ def cfg(**kw):
     dict(mode="baseline", codec="blockquant"), dict(world=3), dict(rank=4, world=4), dict(dt=-1.0),
     dict(region_sharing=False, store="host"), dict(codec=7), dict(codec="trunc16", rate_bits=8),
     dict(codec="zfp", rate_bits=33), dict(codec="zfp", rate_bits=0), dict(decoded_velocity=True, store="host"),
+    dict(mode="baseline", codec="identity", world=2, rank=0),
 ])
 def test_config_errors(kw):
     with pytest.raises(oocs.OocsError) as e:
@@ -250,3 +251,56 @@ def test_binding_structs_mirror_the_header():
     oocs.lib().oocs_abi_sizes(out)
     mine = [ctypes.sizeof(t) for t in (oocs.Config, oocs.Stats, oocs.PlanInfo, oocs.Block, oocs.Op, oocs.Span)]
     assert list(out) == mine
+
+
+# ---- multi-GPU (world > 1): the per-rank schedule with in-library peer sends ------------------------
+@pytest.mark.parametrize("sched", ["alg1", "dag", "dag_func"])
+@pytest.mark.parametrize("mode", ["swb", "dwb", "compress"])
+@pytest.mark.parametrize("world,n,k", [(2, 4, 2), (3, 3, 1), (4, 8, 3)])
+def test_multirank_schedule_race_free_with_sends(world, n, k, mode, sched):
+    """Every rank's op list is race-free over 3 sweeps (the SEND reads the encoded edge planes before the
+    lane's next H2D overwrites them), has no host barrier, and sends each edge once per sweep: the
+    first chunk's lower kR planes to rank-1 (arg bit 0), the last chunk's upper planes to rank+1 (bit 1).
+    Sweeps stay pipelined back to back: the only cross-rank dependencies are device-side flags."""
+    nz = 16 * n
+    for r in range(world):
+        c = cfg(nz=nz * world, n_blocks=n * world, tb_depth=k, mode=mode, schedule=sched, rank=r, world=world)
+        ops, bad = _check(c, 3 * k)
+        assert bad == [], (r, bad[:3])
+        sends = [o for o in ops if o["kind"] == "SEND"]
+        first, last = r * n, (r + 1) * n - 1
+        want = []
+        for t in range(3):
+            for blk in sorted({first, last}):
+                m = (1 if blk == first and r > 0 else 0) | (2 if blk == last and r + 1 < world else 0)
+                if m:
+                    want.append((t, blk, m))
+        assert sorted((o["sweep"], o["block"], o["arg"]) for o in sends) == sorted(want)
+        # the send follows its chunk's encode and precedes its D2H on the same lane
+        for o in sends:
+            lane_ops = [(i, x["kind"]) for i, x in enumerate(ops) if x["g"] == o["g"] and x["kind"] in ("ENCODE", "SEND", "D2H")]
+            assert [k_ for _, k_ in lane_ops] == ["ENCODE", "SEND", "D2H"]
+
+
+def test_multirank_device_store_sends_after_every_sweep():
+    """The device store sends too, after every sweep including the last one (the next oocs_run starts from
+    the neighbours' current edge planes: run(a); run(b) == run(a + b))."""
+    for r in range(3):
+        c = cfg(nz=96, n_blocks=6, tb_depth=2, store="device", rank=r, world=3)
+        ops = oocs.oocs_schedule(c, 2)  # one sweep
+        sends = [(o["block"], o["arg"]) for o in ops if o["kind"] == "SEND"]
+        want = {0: [(1, 2)], 1: [(2, 1), (3, 2)], 2: [(4, 1)]}[r]
+        assert sorted(sends) == want
+
+
+def test_multirank_exchange_region_accounting():
+    """world > 1 adds exactly one exchange region to the device peak -- 256 B of flags plus 2 sides x 2
+    parities x 2 pressures ghost slots of kR planes -- and nothing else (host store: the rank's arena
+    equals a one-rank plan of the same chunk geometry)."""
+    kw = dict(nx=256, ny=256, dt=0.1, tb_depth=4, rate_bits=16)
+    b = oocs.oocs_plan_estimate(cfg(nz=512, n_blocks=8, world=2, rank=1, **kw))
+    one = oocs.oocs_plan_estimate(cfg(nz=256, n_blocks=4, **kw))
+    assert (b.max_ext_planes, b.working_set_bytes, b.staging_bytes) == (one.max_ext_planes, one.working_set_bytes,
+                                                                      one.staging_bytes)
+    slot = _al(4 * oocs.R * b.plane_bytes)
+    assert b.arena_bytes - one.arena_bytes == _al(256 + 8 * slot)
