@@ -323,7 +323,9 @@ oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t 
 oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi);
 
 /* The same two calls with DEVICE memory of the plan's device on the caller's side (same raw layout):
- * state generated or consumed on the GPU never crosses PCIe uncompressed. */
+ * state generated or consumed on the GPU never crosses PCIe uncompressed.  The library works on its own
+ * streams: the caller's writes to `src` must be complete (e.g. its stream synchronized) before the call;
+ * `dst` is complete when the call returns. */
 oocs_status oocs_load_device(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi);
 oocs_status oocs_store_device(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi);
 

@@ -335,6 +335,9 @@ class Plan:
     def load_device(self, array, tensor, a_lo, a_hi):
         """tensor: contiguous float32 CUDA tensor (a_hi-a_lo, ay, ax) on the plan's device."""
         assert tensor.is_cuda and tensor.is_contiguous() and tuple(tensor.shape) == (a_hi - a_lo, self.info.ay, self.info.ax)
+        import torch
+
+        torch.cuda.current_stream(tensor.device).synchronize()  # the library reads on its own streams
         oocs_load_device(self.handle, array, tensor.data_ptr(), a_lo, a_hi)
 
     def store_device(self, array, tensor, a_lo, a_hi):

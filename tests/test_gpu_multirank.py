@@ -152,10 +152,11 @@ def test_split_runs_equal_one_run(args):
 
 
 def test_host_h2d_skips_ghost_pressure_planes():
-    """Out-of-core rank with neighbours on both sides: its pressure halo never crosses PCIe (only the
+    """Out-of-core ranks with neighbours on both sides: their pressure halo never crosses PCIe (only the
     static velocity ghost planes do)."""
     args = ("blockquant", "host", "swb")
-    res = _sharded(args, 3, [K])
+    world = 4
+    res = _sharded(args, world, [K])
     one = oocs.Plan(_cfg(*args))
     pb = one.info.plane_bytes
     one.close()
@@ -166,6 +167,6 @@ def test_host_h2d_skips_ghost_pressure_planes():
         # per sweep: velocity over the store range, pressures over the owned range plus the physical
         # boundary planes the edge ranks own, nothing more
         lo_b = R if rank == 0 else 0
-        hi_b = R if rank == 2 else 0
+        hi_b = R if rank == world - 1 else 0
         assert h2d == ((sh - sl) + 2 * (own + lo_b + hi_b)) * pb, (rank, h2d)
-        assert sh - sl == own + (kR if rank > 0 else R) + (kR if rank < 2 else R)
+        assert sh - sl == own + (kR if rank > 0 else R) + (kR if rank < world - 1 else R)
