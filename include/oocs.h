@@ -51,8 +51,9 @@
 extern "C" {
 #endif
 
-#define OOCS_RADIUS 4      /* 25-point star stencil radius (Table 1 HALO=4) */
-#define OOCS_ABI_VERSION 1
+#define OOCS_RADIUS 4      /* halo width of every grid and chunk extent: the 25-point star's radius (P:L212,
+                              Table 1 HALO=4); every stencil below reaches at most this far */
+#define OOCS_ABI_VERSION 2  /* 2: oocs_config.stencil / v_max / ext_streams, oocs_step's stencil argument */
 
 typedef enum {
     OOCS_OK = 0,
@@ -75,6 +76,18 @@ typedef enum {
                                 * rate_bits must be 16; raw bf16 planes (ax*ay*2 B per plane, x fastest); never
                                 * reports OOCS_ERR_DATA (Inf stays Inf, finite values above the bf16 range round to Inf) */
 } oocs_codec;
+
+/* The stencil of the update p_next = 2 p - p_prev + (v dt)^2 L(p), h = 1 ("25-point stencil ...
+ * acoustic wave propagation").  L is evaluated in difference form (DESIGN.md §3 "stencil
+ * evaluation order").  Both use the same R = 4 halo, plane ranges and temporal-blocking extents (kR planes
+ * per side with R = OOCS_RADIUS): STAR7 needs only 1 plane per step, so its chunks carry a conservative
+ * halo (redundant but exact: blocked == in-core bitwise, DESIGN.md §3 "STAR7 geometry").
+ * CFL limit of the leapfrog (v dt / h at most 2 / sqrt(3 |symbol(pi)|)): ACOUSTIC25 2/sqrt(3*2048/315) =
+ * 0.452856, STAR7 2/sqrt(12) = 0.577350. */
+typedef enum {
+    OOCS_STENCIL_ACOUSTIC25 = 0, /* 2nd order in time, 8th in space: c = (-205/72, 8/5, -1/5, 8/315, -1/560), R = 4 */
+    OOCS_STENCIL_STAR7 = 1       /* 2nd order in space: c = (-2, 1), radius 1: small exact tests */
+} oocs_stencil;
 
 /* Pipeline architectures of the paper (Fig. 6 `fig:3ver`, Fig. 7 `fig:swb`). */
 typedef enum {
@@ -146,6 +159,18 @@ typedef struct {
     int32_t rank, world;      /* z-slab sharding: this process owns a contiguous run of blocks */
     uint32_t flags;           /* OOCS_FLAG_* */
     uint64_t device_capacity; /* 0 = unlimited; else the arena may not exceed this many bytes */
+    /* ---- ABI 2 ---- */
+    int32_t stencil;          /* oocs_stencil */
+    float v_max;              /* declared bound on |v| (0 = undeclared).  oocs_plan_create rejects dt*v_max above
+                               * the stencil's CFL limit; independently, every oocs_load / oocs_load_device of the
+                               * velocity (array 0) measures max|v| of the loaded planes on the GPU and rejects
+                               * dt*max|v| above the limit (OOCS_ERR_CONFIG; NaN velocity counts as above).
+                               * oocs_store_write_raw (trusted checkpoints) is not checked. */
+    void *ext_streams[8];     /* optional caller-owned cudaStream_t per lane (e.g. torch streams): entry l < n_lanes,
+                               * if non-NULL, replaces the library's kernel stream of lane l (its decode, steps and
+                               * encode are issued there, so work the caller queued on it earlier runs first).  The
+                               * library never destroys them; they must outlive the plan and belong to
+                               * cfg->device.  NULL entries: library-owned streams. */
 } oocs_config;
 
 typedef struct {
@@ -237,8 +262,9 @@ typedef struct oocs_plan oocs_plan;
  * (out[cfg->n_blocks], caller-owned).  Pure function of cfg.
  * Errors: OOCS_ERR_CONFIG for nx/ny/nz not multiples of 4, n_blocks > nz/4,
  * k*R >= owned width, rate outside [2,24], world not dividing
- * n_blocks, dt <= 0 or above the CFL limit 2/(v_max*sqrt(19.505...)) is NOT
- * checked here (v is data). */
+ * n_blocks, dt <= 0, unknown stencil, v_max < 0, or dt*v_max above the
+ * stencil's CFL limit when v_max is declared (the velocity data itself is
+ * checked by oocs_load). */
 oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out);
 
 /* Lower the pipeline of `steps` time steps (steps % k == 0) for this rank
@@ -314,8 +340,10 @@ oocs_status oocs_destroy(oocs_plan *plan);
  * (a_hi-a_lo, ay, ax) float32 into the store.  array: 0 = velocity
  * (read-only dataset), 1 = pressure at t-1, 2 = pressure at t.
  * The GPU encodes; host memory is only read during the call.
- * Errors: OOCS_ERR_CONFIG (range), OOCS_ERR_DATA (non-finite input for a
- * lossy codec), OOCS_ERR_CUDA. */
+ * Errors: OOCS_ERR_CONFIG (range; for array 0 also dt*max|v| above the
+ * stencil's CFL limit, see oocs_config.v_max -- the store is then undefined
+ * for those planes), OOCS_ERR_DATA (non-finite input for a lossy codec),
+ * OOCS_ERR_CUDA. */
 oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi);
 
 /* Decompress allocated planes [a_lo, a_hi) of one array into HOST `dst`
@@ -364,13 +392,14 @@ oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int
                         int64_t pitch, int32_t codec, int32_t rate_bits, int32_t *err_flag,
                         void *stream);
 
-/* One leapfrog step of the 25-point stencil:
- *   p_prev[z] <- 2 p_curr[z] - p_prev[z] + (v dt)^2 Lap25(p_curr)[z]
- * on buffer planes [z_lo, z_hi) (R <= z_lo, z_hi <= planes-R), interior x,y.
- * All pointers DEVICE, working-buffer layout.  p_prev is updated in place. */
+/* One leapfrog step of the chosen stencil:
+ *   p_prev[z] <- 2 p_curr[z] - p_prev[z] + (v dt)^2 L(p_curr)[z]
+ * on buffer planes [z_lo, z_hi) (R <= z_lo, z_hi <= planes-R), interior x,y (R = OOCS_RADIUS for both
+ * stencils).  All pointers DEVICE, working-buffer layout.  p_prev is updated in place.  stencil is an
+ * oocs_stencil.  No CFL check (no velocity bound is known here). */
 oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int64_t ax, int64_t ay,
                       int64_t planes, int64_t pitch, float dt, int64_t z_lo, int64_t z_hi,
-                      void *stream);
+                      int32_t stencil, void *stream);
 
 /* ---- misc -------------------------------------------------------------- */
 const char *oocs_last_error(void);

@@ -49,6 +49,10 @@ def lib():
         L.oracle_coeffs.argtypes = [vp]
         L.oracle_step.argtypes = [i64, i64, i64, vp, vp, vp, f32, i64, i64]
         L.oracle_incore.argtypes = [i64, i64, i64, vp, vp, vp, f32, i64]
+        L.oracle_step_s.argtypes = [i32, i64, i64, i64, vp, vp, vp, f32, i64, i64]
+        L.oracle_incore_s.argtypes = [i32, i64, i64, i64, vp, vp, vp, f32, i64]
+        L.oracle_pipeline_s.argtypes = [i32, i64, i64, i64, i64, i64, f32, i64, i32, i32, vp, vp, vp]
+        L.oracle_pipeline_s.restype = i32
         L.oracle_bq_encode_block.argtypes = [vp, i32, vp]
         L.oracle_bq_encode_block.restype = i32
         L.oracle_bq_decode_block.argtypes = [vp, i32, vp]
@@ -102,18 +106,22 @@ def coeffs() -> np.ndarray:
     return c
 
 
-def step(vel, p_prev, p_curr, dt, z_lo, z_hi):
+STENCIL_ACOUSTIC25 = 0
+STENCIL_STAR7 = 1
+
+
+def step(vel, p_prev, p_curr, dt, z_lo, z_hi, stencil=STENCIL_ACOUSTIC25):
     """One leapfrog step on buffer planes [z_lo, z_hi); p_prev is overwritten with p_next."""
     planes, ay, ax = p_curr.shape
     for a in (vel, p_prev, p_curr):
         assert a.dtype == np.float32 and a.shape == (planes, ay, ax)
-    lib().oracle_step(ax, ay, planes, _p(vel), _p(p_prev), _p(p_curr), float(dt), z_lo, z_hi)
+    lib().oracle_step_s(stencil, ax, ay, planes, _p(vel), _p(p_prev), _p(p_curr), float(dt), z_lo, z_hi)
 
 
-def incore(vel, p_prev, p_curr, dt, steps):
+def incore(vel, p_prev, p_curr, dt, steps, stencil=STENCIL_ACOUSTIC25):
     """T plain steps in place; returns (p_prev, p_curr) = levels (T-1, T)."""
     az, ay, ax = p_curr.shape
-    lib().oracle_incore(ax, ay, az, _p(vel), _p(p_prev), _p(p_curr), float(dt), steps)
+    lib().oracle_incore_s(stencil, ax, ay, az, _p(vel), _p(p_prev), _p(p_curr), float(dt), steps)
     return p_prev, p_curr
 
 
@@ -162,10 +170,10 @@ def plan(nz, n, k, sharing=True) -> np.ndarray:
     return out
 
 
-def pipeline(ax, ay, nz, n, k, dt, steps, codec, q, S_vel, S_prev, S_curr):
+def pipeline(ax, ay, nz, n, k, dt, steps, codec, q, S_vel, S_prev, S_curr, stencil=STENCIL_ACOUSTIC25):
     """Run the method on compressed stores in place (S_prev/S_curr updated)."""
-    rc = lib().oracle_pipeline(ax, ay, nz, n, k, float(dt), steps, codec, q,
-                               _p(S_vel), _p(S_prev), _p(S_curr))
+    rc = lib().oracle_pipeline_s(stencil, ax, ay, nz, n, k, float(dt), steps, codec, q,
+                                 _p(S_vel), _p(S_prev), _p(S_curr))
     if rc:
         raise OracleError(rc)
     return S_prev, S_curr

@@ -18,6 +18,9 @@
  *                            stencil over a plane range, fp64 arithmetic,
  *                            fp32 storage ("25-point stencil ... acoustic
  *                            wave propagation")
+ *   oracle_step7             the same step with the 2nd-order 7-point Laplacian (STAR7,
+ *                            small exact tests); oracle_step_s / _incore_s /
+ *                            _pipeline_s take the stencil (0 = 25-point, 1 = STAR7)
  *   oracle_incore            T plain steps over the whole interior
  *   oracle_bq_encode_block / oracle_bq_decode_block
  *                            fixed-rate BlockQuant codec on one 4x4x4 block
@@ -132,14 +135,49 @@ void oracle_step(int64_t ax, int64_t ay, int64_t planes, const float *vel,
     }
 }
 
+/* STAR7 (oocs.h OOCS_STENCIL_STAR7, SURVEY §8(b) "STAR7 (R=1) for small exact tests"): the same leapfrog
+ * with the textbook 2nd-order 7-point Laplacian,
+ *   Lap7 = sum over axes x,y,z of [f(+1) + f(-1) - 2 f0],  h = 1,
+ * on the same allocated layout (R = 4 halo; only the first halo cell is read).  Binary64 arithmetic,
+ * stored as binary32. */
+void oracle_step7(int64_t ax, int64_t ay, int64_t planes, const float *vel, float *p_prev,
+                  const float *p_curr, float dt, int64_t z_lo, int64_t z_hi) {
+    const int64_t sy = ax, sz = ax * ay;
+    (void)planes;
+#pragma omp parallel for schedule(static)
+    for (int64_t z = z_lo; z < z_hi; ++z) {
+        for (int64_t y = R; y < ay - R; ++y) {
+            for (int64_t x = R; x < ax - R; ++x) {
+                const int64_t i = z * sz + y * sy + x;
+                const double f0 = p_curr[i];
+                double lap = 0.0;
+                lap += (double)p_curr[i + 1] + (double)p_curr[i - 1] - 2.0 * f0;
+                lap += (double)p_curr[i + sy] + (double)p_curr[i - sy] - 2.0 * f0;
+                lap += (double)p_curr[i + sz] + (double)p_curr[i - sz] - 2.0 * f0;
+                const double vdt = (double)vel[i] * (double)dt;
+                p_prev[i] = (float)(2.0 * f0 - (double)p_prev[i] + vdt * vdt * lap);
+            }
+        }
+    }
+}
+
+/* stencil 0 = the 25-point acoustic stencil (oracle_step), 1 = STAR7 (oracle_step7) */
+void oracle_step_s(int stencil, int64_t ax, int64_t ay, int64_t planes, const float *vel,
+                   float *p_prev, const float *p_curr, float dt, int64_t z_lo, int64_t z_hi) {
+    if (stencil == 1)
+        oracle_step7(ax, ay, planes, vel, p_prev, p_curr, dt, z_lo, z_hi);
+    else
+        oracle_step(ax, ay, planes, vel, p_prev, p_curr, dt, z_lo, z_hi);
+}
+
 /* T plain steps over the whole interior.  Dirichlet boundary:
  * the R-cell halo on all six faces keeps its initial values.
  * On return p_prev holds time level T-1 and p_curr level T. */
-void oracle_incore(int64_t ax, int64_t ay, int64_t az, const float *vel,
-                   float *p_prev, float *p_curr, float dt, int64_t steps) {
+void oracle_incore_s(int stencil, int64_t ax, int64_t ay, int64_t az, const float *vel,
+                     float *p_prev, float *p_curr, float dt, int64_t steps) {
     float *a = p_prev, *b = p_curr; /* a = level t-1, b = level t */
     for (int64_t t = 0; t < steps; ++t) {
-        oracle_step(ax, ay, az, vel, a, b, dt, R, az - R); /* a <- level t+1 */
+        oracle_step_s(stencil, ax, ay, az, vel, a, b, dt, R, az - R); /* a <- level t+1 */
         float *tmp = a;
         a = b;
         b = tmp;
@@ -152,6 +190,11 @@ void oracle_incore(int64_t ax, int64_t ay, int64_t az, const float *vel,
         memcpy(p_prev, tmp, n * sizeof(float));
         free(tmp);
     }
+}
+
+void oracle_incore(int64_t ax, int64_t ay, int64_t az, const float *vel,
+                   float *p_prev, float *p_curr, float dt, int64_t steps) {
+    oracle_incore_s(0, ax, ay, az, vel, p_prev, p_curr, dt, steps);
 }
 
 /* ------------------------------------------------------------------ */
@@ -389,9 +432,9 @@ int oracle_plan(int64_t nz, int64_t n, int64_t k, int sharing, int64_t *out) {
  * S:L102).  Region sharing only changes which bytes cross PCIe, not values,
  * so the oracle has no notion of it.
  * steps must be a multiple of k.  Returns ORACLE_OK or an error. */
-int oracle_pipeline(int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k, float dt,
-                    int64_t steps, int codec, int q, const uint8_t *S_vel, uint8_t *S_prev,
-                    uint8_t *S_curr) {
+int oracle_pipeline_s(int stencil, int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k,
+                      float dt, int64_t steps, int codec, int q, const uint8_t *S_vel,
+                      uint8_t *S_prev, uint8_t *S_curr) {
     if (k < 1 || steps % k) return ORACLE_ERR_CONFIG;
     int64_t *plan = (int64_t *)malloc((size_t)n * 8 * sizeof(int64_t));
     int rc = oracle_plan(nz, n, k, 1, plan);
@@ -426,7 +469,7 @@ int oracle_pipeline(int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k, fl
                  * except at the physical boundary (Fig. 1(b)) */
                 const int64_t lo = (ext_lo == -R) ? 0 : ext_lo + s * R;
                 const int64_t hi = (ext_hi == nz + R) ? nz : ext_hi - s * R;
-                oracle_step(ax, ay, E, v, prev, curr, dt, lo - ext_lo, hi - ext_lo);
+                oracle_step_s(stencil, ax, ay, E, v, prev, curr, dt, lo - ext_lo, hi - ext_lo);
                 float *t = prev;
                 prev = curr;
                 curr = t;
@@ -448,6 +491,12 @@ int oracle_pipeline(int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k, fl
     free(N_curr);
     free(plan);
     return rc;
+}
+
+int oracle_pipeline(int64_t ax, int64_t ay, int64_t nz, int64_t n, int64_t k, float dt,
+                    int64_t steps, int codec, int q, const uint8_t *S_vel, uint8_t *S_prev,
+                    uint8_t *S_curr) {
+    return oracle_pipeline_s(0, ax, ay, nz, n, k, dt, steps, codec, q, S_vel, S_prev, S_curr);
 }
 
 /* ------------------------------------------------------------------ */

@@ -38,6 +38,7 @@ CODEC = {"identity": 0, "blockquant": 1, "zfp": 2, "trunc16": 3}
 MODE = {"baseline": 0, "compress": 1, "swb": 2, "dwb": 3}
 STORE = {"host": 0, "device": 1}
 SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}
+STENCIL = {"acoustic25": 0, "star7": 1}
 FLAG_PROFILE = 1
 FLAG_RESIDENT_VELOCITY = 2
 FLAG_FUSE_ENCODE = 4
@@ -58,7 +59,9 @@ class Config(ctypes.Structure):
     _fields_ = [("struct_size", u32), ("nx", i64), ("ny", i64), ("nz", i64), ("dt", f32),
                 ("n_blocks", i32), ("tb_depth", i32), ("codec", i32), ("rate_bits", i32), ("mode", i32),
                 ("region_sharing", i32), ("n_lanes", i32), ("schedule", i32), ("store", i32), ("device", i32), ("rank", i32), ("world", i32),
-                ("flags", u32), ("device_capacity", u64)]
+                ("flags", u32), ("device_capacity", u64),
+                # ABI 2
+                ("stencil", i32), ("v_max", f32), ("ext_streams", vp * 8)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -137,7 +140,7 @@ def lib():
             "oocs_timeline": ([vp, vp, i64, P(i64)], i32),
             "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
             "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
-            "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, vp], i32),
+            "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, i32, vp], i32),
             "oocs_last_error": ([], ctypes.c_char_p),
             "oocs_abi_version": ([], i32),
             "oocs_abi_sizes": ([vp], None),
@@ -158,7 +161,9 @@ def _check(st: int, where: str):
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
                 device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False,
-                timeline=False, executor="dispatch", decoded_velocity=False) -> Config:
+                timeline=False, executor="dispatch", decoded_velocity=False, stencil="acoustic25", v_max=0.0,
+                ext_streams=()) -> Config:
+    """ext_streams: up to 8 integer cudaStream_t handles (e.g. torch.cuda.Stream().cuda_stream), lane order."""
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
     c.nx, c.ny, c.nz = nx, ny, nz
@@ -176,6 +181,11 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
                | (FLAG_TIMELINE if timeline else 0) | EXECUTOR[executor]
                | (FLAG_FUSE_ENCODE if fusion else 0) | (FLAG_DECODED_VELOCITY if decoded_velocity else 0))
     c.device_capacity = device_capacity
+    c.stencil = STENCIL[stencil] if isinstance(stencil, str) else stencil
+    c.v_max = float(v_max)
+    assert len(ext_streams) <= 8
+    for i, h in enumerate(ext_streams):
+        c.ext_streams[i] = h or None
     return c
 
 
@@ -310,8 +320,10 @@ def oocs_encode(src_ptr: int, dst_ptr: int, ax, ay, planes, pitch, codec, rate_b
                              stream or None), "oocs_encode")
 
 
-def oocs_step(vel_ptr: int, pprev_ptr: int, pcurr_ptr: int, ax, ay, planes, pitch, dt, z_lo, z_hi, stream=0):
-    _check(lib().oocs_step(vel_ptr, pprev_ptr, pcurr_ptr, ax, ay, planes, pitch, float(dt), z_lo, z_hi,
+def oocs_step(vel_ptr: int, pprev_ptr: int, pcurr_ptr: int, ax, ay, planes, pitch, dt, z_lo, z_hi, stream=0, *,
+              stencil="acoustic25"):
+    st = STENCIL[stencil] if isinstance(stencil, str) else stencil
+    _check(lib().oocs_step(vel_ptr, pprev_ptr, pcurr_ptr, ax, ay, planes, pitch, float(dt), z_lo, z_hi, st,
                            stream or None), "oocs_step")
 
 

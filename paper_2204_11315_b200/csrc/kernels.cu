@@ -1346,10 +1346,75 @@ static cudaError_t launch_stencil(const float *vel, float *pprev, const float *p
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// STAR7 (oocs_stencil 1): the 2nd-order 7-point Laplacian, radius 1, for small exact tests.
+// Not a hot path: one thread per (x, y) column of a 32 x 8 tile marching over its z range with the
+// z-neighbours in registers, x/y neighbours through L1.  Difference form as the 25-point kernel:
+//   L = ((f(x-1)+f(x+1)) - 2 f0) + ((f(y-1)+f(y+1)) - 2 f0) + ((f(z-1)+f(z+1)) - 2 f0)  (left to right)
+//   p_next = (v dt)^2 L + (2 f0 - p_prev)  (one FMA)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) star7_step_kernel(const float *__restrict__ vel, float *pprev,
+                                                         const float *__restrict__ pcurr, int nx, int ny, int z_lo,
+                                                         int z_hi, int zchunk, int64_t pitch, int64_t pstride,
+                                                         float dt) {
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    if (x >= nx || y >= ny) return;
+    const int zs = z_lo + blockIdx.z * zchunk, ze = min(z_hi, zs + zchunk);
+    const int64_t g = (int64_t)(y + R) * pitch + x + R + XOFF;
+    float fm = __ldg(pcurr + (int64_t)(zs - 1) * pstride + g);
+    float f0 = zs < ze ? __ldg(pcurr + (int64_t)zs * pstride + g) : 0.f;
+    for (int z = zs; z < ze; ++z) {
+        const int64_t i = (int64_t)z * pstride + g;
+        const float fp = __ldg(pcurr + i + pstride);
+        const float f2 = __fadd_rn(f0, f0);
+        const float dx = __fsub_rn(__fadd_rn(__ldg(pcurr + i - 1), __ldg(pcurr + i + 1)), f2);
+        const float dy = __fsub_rn(__fadd_rn(__ldg(pcurr + i - pitch), __ldg(pcurr + i + pitch)), f2);
+        const float dz = __fsub_rn(__fadd_rn(fm, fp), f2);
+        const float lap = __fadd_rn(__fadd_rn(dx, dy), dz);
+        const float vd = __fmul_rn(__ldg(vel + i), dt);
+        pprev[i] = __fmaf_rn(__fmul_rn(vd, vd), lap, __fsub_rn(f2, pprev[i]));
+        fm = f0;
+        f0 = fp;
+    }
+}
+
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
-                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st) {
+                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int stencil, cudaStream_t st) {
+    if (stencil == OOCS_STENCIL_STAR7) {
+        if (z_hi <= z_lo) return cudaSuccess;
+        const int nx = (int)(ax - 2 * R), ny = (int)(ay - 2 * R), Z = (int)(z_hi - z_lo);
+        const int tiles = ((nx + 31) / 32) * ((ny + 7) / 8);
+        const int nzc = std::max(1, std::min(Z, (148 * 8 + tiles - 1) / tiles));
+        const int zchunk = (Z + nzc - 1) / nzc;
+        const dim3 grid((nx + 31) / 32, (ny + 7) / 8, (Z + zchunk - 1) / zchunk);
+        star7_step_kernel<<<grid, dim3(32, 8), 0, st>>>(vel, pprev, pcurr, nx, ny, (int)z_lo, (int)z_hi, zchunk, pitch,
+                                                         ay * pitch, dt);
+        return cudaGetLastError();
+    }
     StepArgs a{};
     return launch_stencil<16, ENC_NONE>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+}
+
+// max |x| over rows of n floats (CFL check of a loaded velocity); float bits of non-negative values order
+// like unsigned integers, and NaN's bits exceed +Inf's
+__global__ void __launch_bounds__(256) absmax_kernel(const float *__restrict__ src, int64_t rows, int64_t n,
+                                                     int64_t pitch, uint32_t *out) {
+    uint32_t m = 0;
+    const int64_t total = rows * n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / n, c = i - r * n;
+        m = max(m, __float_as_uint(src[r * pitch + c]) & 0x7fffffffu);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+cudaError_t launch_absmax(const float *src, int64_t rows, int64_t n, int64_t pitch, uint32_t *out, cudaStream_t st) {
+    if (rows <= 0 || n <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>(148 * 8, (rows * n + 255) / 256);
+    absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, rows, n, pitch, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,

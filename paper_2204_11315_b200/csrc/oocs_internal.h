@@ -15,6 +15,10 @@ constexpr int XOFF = 32 - R;  // column offset: interior x = R lands on a 128-by
 constexpr int N_ARRAYS = 3;   // 0 velocity (read-only), 1 pressure t-1, 2 pressure t
 constexpr int MAX_LANES = 8;  // strm[0:3] in the paper; configurable 2..8
 
+// CFL limit of the leapfrog, v dt / h <= 2 / sqrt(3 |L1(pi)|), with L1(pi) = c0 + 2 sum_m (-1)^m c_m the 1-D
+// operator's symbol at the Nyquist wavenumber: ACOUSTIC25 |L1(pi)| = 2048/315, STAR7 4 (oocs.h oocs_stencil)
+inline double cfl_limit(int stencil) { return stencil == OOCS_STENCIL_STAR7 ? 0.5773502691896258 : 0.4528555233184199; }
+
 // Geometry derived from a config (pure host; plan.cpp).
 struct Geometry {
     oocs_config cfg;
@@ -45,7 +49,10 @@ cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, 
 cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, int64_t ax, int64_t ay,
                           int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
-                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, cudaStream_t st);
+                        int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int stencil, cudaStream_t st);
+// max |x| over `rows` rows of `n` floats (row stride `pitch` floats) folded into *out (float bits as u32,
+// atomicMax; NaN compares above +Inf); *out must be initialised by the caller
+cudaError_t launch_absmax(const float *src, int64_t rows, int64_t n, int64_t pitch, uint32_t *out, cudaStream_t st);
 // last step fused with the BlockQuant encode of the owned slabs [z_lo, z_hi) (device store)
 cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,
                                int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,

@@ -24,6 +24,11 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->nx <= 0 || c->ny <= 0 || c->nz <= 0) return bad(err, "grid dimensions must be positive");
     if (c->nx % 4 || c->ny % 4 || c->nz % 4) return bad(err, "nx, ny, nz must be multiples of 4 (4x4x4 codec blocks)");
     if (!(c->dt > 0.0f) || !std::isfinite(c->dt)) return bad(err, "dt must be positive and finite");
+    if (c->stencil != OOCS_STENCIL_ACOUSTIC25 && c->stencil != OOCS_STENCIL_STAR7) return bad(err, "unknown stencil");
+    if (!(c->v_max >= 0.0f) || !std::isfinite(c->v_max)) return bad(err, "v_max must be finite and >= 0 (0 = undeclared)");
+    if ((double)c->dt * (double)c->v_max > cfl_limit(c->stencil))
+        return bad(err, "dt * v_max exceeds the stencil's CFL limit (" + std::to_string(cfl_limit(c->stencil)) +
+                            "; DESIGN.md Q1)");
     if (c->codec != OOCS_CODEC_IDENTITY && c->codec != OOCS_CODEC_BLOCKQUANT && c->codec != OOCS_CODEC_ZFP &&
         c->codec != OOCS_CODEC_TRUNC16)
         return bad(err, "unknown codec");

@@ -69,6 +69,8 @@ struct Plan {
     bool connected = false;
     int64_t seq = 0;                        // index t of the state S_t the store holds (sweeps so far)
     int *d_err = nullptr;
+    uint32_t *d_vmax = nullptr;           // oocs_load of the velocity: max|v| of the loaded planes (float bits)
+    bool ext_klane[MAX_LANES] = {};       // lane's kernel stream is the caller's (oocs_config.ext_streams)
     cudaStream_t lanes[MAX_LANES] = {};   // copy stream of each lane (and its kernels with LANE_SINGLE_STREAM)
     cudaStream_t klanes[MAX_LANES] = {};  // kernel stream of each lane (== lanes[] with LANE_SINGLE_STREAM)
     cudaEvent_t xfer_ev[MAX_LANES] = {}, kdone[MAX_LANES] = {};
@@ -289,7 +291,8 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
                           cudaStream_t st, oocs_stats *stats) {
     KernelTiming *t = timing_slot(p, 1);
     if (t) CU(cudaEventRecord(t->a, st));
-    CU(launch_step(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi, p->geo.cfg.dt, st));
+    CU(launch_step(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi, p->geo.cfg.dt,
+                   p->geo.cfg.stencil, st));
     if (t) CU(cudaEventRecord(t->b, st));
     if (stats) {
         stats->kernel_launches[1]++;
@@ -303,7 +306,8 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
 // device store + BlockQuant, opted in: the last step of a chunk is fused with the encode
 static bool fuse_last_step(const Plan *p) {
     const Geometry &g = p->geo;
-    return !g.host_store && g.codec == OOCS_CODEC_BLOCKQUANT && (g.cfg.flags & OOCS_FLAG_FUSE_ENCODE);
+    return !g.host_store && g.codec == OOCS_CODEC_BLOCKQUANT && (g.cfg.flags & OOCS_FLAG_FUSE_ENCODE) &&
+           g.cfg.stencil == OOCS_STENCIL_ACOUSTIC25;
 }
 
 static oocs_status k_step_encode(Plan *p, const float *v, const float *pp, const float *pc, int64_t zlo, int64_t zhi,
@@ -337,12 +341,12 @@ static void free_plan(Plan *p) {
     }
     for (auto e : p->op_done) cudaEventDestroy(e);
     for (int l = 0; l < MAX_LANES; ++l) {
-        if (p->split && p->klanes[l]) cudaStreamDestroy(p->klanes[l]);
+        if (p->split && p->klanes[l] && !p->ext_klane[l]) cudaStreamDestroy(p->klanes[l]);
         if (p->xfer_ev[l]) cudaEventDestroy(p->xfer_ev[l]);
         if (p->kdone[l]) cudaEventDestroy(p->kdone[l]);
     }
-    for (auto &s : p->lanes)
-        if (s) cudaStreamDestroy(s);
+    for (int l = 0; l < MAX_LANES; ++l)
+        if (p->lanes[l] && (p->split || !p->ext_klane[l])) cudaStreamDestroy(p->lanes[l]);
     for (auto &v : p->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : p->lane_done)
@@ -499,7 +503,8 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
     }
     if (p->resident_vel) p->dvel = (uint8_t *)p->arena.take(arr_store);
     if (z.vdec) p->vdec = (float *)p->arena.take(z.vdec);
-    p->d_err = (int *)p->arena.take(sizeof(int));
+    p->d_err = (int *)p->arena.take(2 * sizeof(int));
+    p->d_vmax = p->d_err ? reinterpret_cast<uint32_t *>(p->d_err + 1) : nullptr;
     if (!p->d_err) {
         set_error("internal: arena carve-out overflow");
         free_plan(p);
@@ -553,15 +558,29 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
         p->copy_chunk = env ? (uint64_t)(std::strtod(env, nullptr) * 1048576.0) & ~uint64_t(15) : 0;
     }
     for (int l = 0; l < g.lanes; ++l) {
-        if (cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess ||
+        // a caller stream (oocs_config.ext_streams) is the lane's kernel stream (its only stream with
+        // LANE_SINGLE_STREAM); it must belong to the plan's device
+        cudaStream_t ext = static_cast<cudaStream_t>(g.cfg.ext_streams[l]);
+        if (ext) {
+            int sdev = -1;
+            if (cudaStreamGetDevice(ext, &sdev) != cudaSuccess || sdev != g.cfg.device) {
+                cudaGetLastError();
+                set_error("ext_streams[" + std::to_string(l) + "] is not a stream of the plan's device");
+                free_plan(p);
+                return OOCS_ERR_CONFIG;
+            }
+            p->ext_klane[l] = true;
+        }
+        if ((!(ext && !p->split) && cudaStreamCreateWithFlags(&p->lanes[l], cudaStreamNonBlocking) != cudaSuccess) ||
             cudaEventCreateWithFlags(&p->lane_done[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->xfer_ev[l], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->kdone[l], cudaEventDisableTiming) != cudaSuccess ||
-            (p->split && cudaStreamCreateWithFlags(&p->klanes[l], cudaStreamNonBlocking) != cudaSuccess)) {
+            (p->split && !ext && cudaStreamCreateWithFlags(&p->klanes[l], cudaStreamNonBlocking) != cudaSuccess)) {
             set_error("stream/event creation failed");
             free_plan(p);
             return OOCS_ERR_CUDA;
         }
+        if (ext) (p->split ? p->klanes[l] : p->lanes[l]) = ext;
         if (!p->split) p->klanes[l] = p->lanes[l];
     }
     p->ev_ring = g.nb() + 8;
@@ -1190,13 +1209,14 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
     cudaStream_t s = p->lanes[0];
     const int64_t chunk = g.max_ext / 4 * 4;
     float *ws = p->ws[0][0];
-    CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), s));
+    CU(cudaMemsetAsync(p->d_err, 0, 2 * sizeof(int), s));  // error flag and max|v|
     // staging for the compressed result (host store): reuse a slice of ws[0][1]
     uint8_t *stage = reinterpret_cast<uint8_t *>(p->ws[0][1]);
     for (int64_t a = a_lo; a < a_hi; a += chunk) {
         const int64_t n = std::min(chunk, a_hi - a);
         CU(copy_raw_to_ws(ws, src + (a - a_lo) * g.ax * g.ay, g, n,
                           dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        if (array == 0) CU(launch_absmax(ws + XOFF, n * g.ay, g.ax, g.pitch, p->d_vmax, s));  // CFL check below
         const int64_t z = a - R;
         if (pitched_store(g)) {  // BASELINE: the store holds working-buffer rows
             CU(cudaMemcpyAsync(p->hstore[array] + hoff(p, z), ws, n * spb(p), cudaMemcpyDeviceToHost, s));
@@ -1220,11 +1240,20 @@ static oocs_status load(Plan *p, int32_t array, const float *src, int64_t a_lo, 
         CU(cudaStreamSynchronize(s));
     }
     if (oocs_status r = sync_ghosts(p, array, a_lo, a_hi, true)) return r;
-    int herr = 0;
-    CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (herr) {
+    int herr[2] = {0, 0};
+    CU(cudaMemcpy(herr, p->d_err, sizeof(herr), cudaMemcpyDeviceToHost));
+    if (herr[0]) {
         set_error("oocs_load: non-finite or |x| >= 2^126 value for a lossy codec (S:L200)");
         return OOCS_ERR_DATA;
+    }
+    if (array == 0) {
+        float vmax;
+        std::memcpy(&vmax, &herr[1], sizeof(vmax));
+        if (!((double)g.cfg.dt * (double)vmax <= cfl_limit(g.cfg.stencil))) {  // NaN fails too
+            set_error("oocs_load: dt * max|v| = " + std::to_string((double)g.cfg.dt * vmax) +
+                      " exceeds the stencil's CFL limit " + std::to_string(cfl_limit(g.cfg.stencil)) + " (DESIGN.md Q1)");
+            return OOCS_ERR_CONFIG;
+        }
     }
     return OOCS_OK;
 }
@@ -1585,12 +1614,13 @@ oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int
 }
 
 oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int64_t ax, int64_t ay, int64_t planes,
-                      int64_t pitch, float dt, int64_t z_lo, int64_t z_hi, void *stream) {
-    if (ax % 4 || ay % 4 || pitch < ax + XOFF || pitch % 32 || z_lo < R || z_hi > planes - R || z_lo > z_hi) {
-        set_error("oocs_step: bad geometry or plane range");
+                      int64_t pitch, float dt, int64_t z_lo, int64_t z_hi, int32_t stencil, void *stream) {
+    if (ax % 4 || ay % 4 || pitch < ax + XOFF || pitch % 32 || z_lo < R || z_hi > planes - R || z_lo > z_hi ||
+        (stencil != OOCS_STENCIL_ACOUSTIC25 && stencil != OOCS_STENCIL_STAR7)) {
+        set_error("oocs_step: bad geometry, plane range or stencil");
         return OOCS_ERR_CONFIG;
     }
-    CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, planes, z_lo, z_hi, dt, (cudaStream_t)stream));
+    CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, planes, z_lo, z_hi, dt, stencil, (cudaStream_t)stream));
     return OOCS_OK;
 }
 

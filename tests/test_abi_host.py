@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(oocs.LIB_PATH)
     for n in sorted(names):
         assert hasattr(L, n), n
-    assert oocs.lib().oocs_abi_version() == 1
+    assert oocs.lib().oocs_abi_version() == 2
 
 
 def cfg(**kw):
@@ -43,11 +43,24 @@ def cfg(**kw):
     dict(region_sharing=False, store="host"), dict(codec=7), dict(codec="trunc16", rate_bits=8),
     dict(codec="zfp", rate_bits=33), dict(codec="zfp", rate_bits=0), dict(decoded_velocity=True, store="host"),
     dict(mode="baseline", codec="identity", world=2, rank=0),
+    dict(stencil=2), dict(v_max=-1.0), dict(v_max=float("nan")),
+    dict(dt=0.1, v_max=4.53),            # 0.453 > 2/sqrt(3*2048/315) = 0.45286 (ACOUSTIC25 CFL, Q1)
+    dict(dt=0.1, v_max=5.78, stencil="star7"),  # 0.578 > 2/sqrt(12) = 0.57735
 ])
 def test_config_errors(kw):
     with pytest.raises(oocs.OocsError) as e:
         oocs.oocs_plan_table(cfg(**kw))
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("stencil,vdt", [("acoustic25", 0.4528), ("star7", 0.4529), ("star7", 0.5773)])
+def test_cfl_limit_accepts_below(stencil, vdt):
+    # the limits are 2/sqrt(3 |L1(pi)|): 25-point |L1(pi)| = 2048/315 (exact rationals), 7-point 4
+    from fractions import Fraction
+    sym25 = Fraction(205, 72) + 2 * (Fraction(8, 5) + Fraction(1, 5) + Fraction(8, 315) + Fraction(1, 560))
+    assert sym25 == Fraction(2048, 315)
+    assert vdt < 2 / (3 * float(sym25 if stencil == "acoustic25" else 4)) ** 0.5
+    oocs.oocs_plan_table(cfg(dt=0.1, v_max=vdt / 0.1, stencil=stencil))
 
 
 def test_struct_size_is_checked():
