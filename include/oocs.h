@@ -401,6 +401,20 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
                       int64_t planes, int64_t pitch, float dt, int64_t z_lo, int64_t z_hi,
                       int32_t stencil, void *stream);
 
+/* Two leapfrog steps of the 25-point stencil fused in one pass (NEXT-2 temporal register blocking; the
+ * paper's future work "optimizing GPU computation"), OUT of place:
+ *   C <- p(t+1) = 2 B - A + (v dt)^2 Lap25(B)   on buffer planes [z1_lo, z1_hi)
+ *   D <- p(t+2) = 2 C - B + (v dt)^2 Lap25(C)   on buffer planes [z2_lo, z2_hi)
+ * with A = p(t-1), B = p(t), interior x, y; bitwise equal to two oocs_step calls.  HBM per update pair:
+ * read A, B, v, write C, D (10 B per cell-update vs 16).  Requires R <= z1_lo <= z2_lo <= z1_lo + R and
+ * z2_hi <= z1_hi <= z2_hi + R, z1_hi <= planes - R; level t+1 outside [z1_lo, z1_hi) (in step 2's
+ * reach) is taken from B (a Dirichlet boundary plane).  C and D are written on interior cells only:
+ * their x/y halo and boundary planes are the caller's (the same values as B's for a Dirichlet run).
+ * All pointers DEVICE, working-buffer layout, A/B/V distinct from C/D.  Errors: OOCS_ERR_CONFIG. */
+oocs_status oocs_step2(const float *vel, const float *A, const float *B, float *C, float *D, int64_t ax, int64_t ay,
+                       int64_t planes, int64_t pitch, float dt, int64_t z1_lo, int64_t z1_hi, int64_t z2_lo,
+                       int64_t z2_hi, void *stream);
+
 /* ---- misc -------------------------------------------------------------- */
 const char *oocs_last_error(void);
 int32_t oocs_abi_version(void);

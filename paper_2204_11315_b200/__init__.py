@@ -22,7 +22,7 @@ __all__ = [
     "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
     "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
     "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_load_device", "oocs_store_device", "oocs_store_read_raw",
-    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
+    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step", "oocs_step2",
     "oocs_peer_handle", "oocs_peer_connect", "PEER_HANDLE_BYTES", "Plan", "XOFF", "pitch_for",
 ]
 
@@ -141,6 +141,7 @@ def lib():
             "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
             "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
             "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, i32, vp], i32),
+            "oocs_step2": ([vp, vp, vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, i64, i64, vp], i32),
             "oocs_last_error": ([], ctypes.c_char_p),
             "oocs_abi_version": ([], i32),
             "oocs_abi_sizes": ([vp], None),
@@ -325,6 +326,12 @@ def oocs_step(vel_ptr: int, pprev_ptr: int, pcurr_ptr: int, ax, ay, planes, pitc
     st = STENCIL[stencil] if isinstance(stencil, str) else stencil
     _check(lib().oocs_step(vel_ptr, pprev_ptr, pcurr_ptr, ax, ay, planes, pitch, float(dt), z_lo, z_hi, st,
                            stream or None), "oocs_step")
+
+
+def oocs_step2(vel_ptr: int, a_ptr: int, b_ptr: int, c_ptr: int, d_ptr: int, ax, ay, planes, pitch, dt, z1_lo, z1_hi,
+               z2_lo, z2_hi, stream=0):
+    _check(lib().oocs_step2(vel_ptr, a_ptr, b_ptr, c_ptr, d_ptr, ax, ay, planes, pitch, float(dt), z1_lo, z1_hi, z2_lo,
+                            z2_hi, stream or None), "oocs_step2")
 
 
 @dataclass

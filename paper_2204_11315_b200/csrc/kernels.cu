@@ -64,12 +64,7 @@ struct Xpose {
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 
 // (float)code + 0.5f without the quarter-rate I2F: 2^23 + code is the bit pattern 0x4B000000 | code
-// (code < 2^23), and subtracting 2^23 - 0.5 (representable) is exact (Sterbenz)
-// (two codes at once, paired fp32)
-__device__ __forceinline__ float2 bin_centre2(uint32_t c0, uint32_t c1) {
-    return __fadd2_rn(make_float2(__uint_as_float(0x4B000000u | c0), __uint_as_float(0x4B000000u | c1)),
-                      make_float2(-8388607.5f, -8388607.5f));
-}
+// (code < 2^23), and subtracting 2^23 - 0.5 (representable) is exact (Sterbenz) -- bq_decode_kernel
 // paired fp32 add rounded toward -inf (FADD2.RM)
 __device__ __forceinline__ float2 fadd2_rd(float2 a, float2 b) {
     unsigned long long ua, ub, ur;
@@ -81,6 +76,31 @@ __device__ __forceinline__ float2 fadd2_rd(float2 a, float2 b) {
     return r;
 }
 
+// three-input min / max that propagate NaN (FMNMX3.NAN, sm_100): a block's min and max are NaN iff one
+// of its values is, so the encoder's NaN check rides on the statistics it needs anyway
+__device__ __forceinline__ float min3n(float a, float b, float c) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max3n(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float min2n(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float max2n(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+// bin-centre patterns of the low / high 16-bit code of a packed word: bytes [c0 c1 00 4B] = 2^23 + code
+__device__ __forceinline__ uint32_t pat_lo(uint32_t w) { return __byte_perm(w, 0x4B000000u, 0x7410); }
+__device__ __forceinline__ uint32_t pat_hi(uint32_t w) { return __byte_perm(w, 0x4B000000u, 0x7432); }
 
 // Warp task = one 128-byte line segment of 16 rows (4 y x 4 z) of a
 // 4-plane slab: the blocks bx in [max(0,8L-7), min(nbx-1,8L)] whose columns
@@ -154,14 +174,13 @@ bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const uint32_t y0 = X(w0[i]);
-        uint32_t c_lo = y0 & 0xFFFFu, c_hi = y0 >> 16;
         if (TWO) {
             const uint32_t y1 = X(w1[i]);
-            c_lo |= (y1 & 0xFFFFu) << 16;
-            c_hi |= (y1 >> 16) << 16;
+            cw[i][lane] = (y0 & 0xFFFFu) | ((y1 & 0xFFFFu) << 16);
+            cw[i][lane + 32] = (y0 >> 16) | ((y1 >> 16) << 16);
+        } else {
+            cw[i][lane] = y0;  // packed: low half = code lane, high half = code lane + 32
         }
-        cw[i][lane] = c_lo;
-        cw[i][lane + 32] = c_hi;
     }
     __syncwarp();
     // reconstruct in the store layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12 (code j = xi + 4r),
@@ -169,16 +188,33 @@ bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
     const int ib = lane & 7, r0 = lane >> 3;
     const float mn = __shfl_sync(0xffffffffu, mn_l, ib), step = __shfl_sync(0xffffffffu, step_l, ib);
     float *dbase = dst + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
+    const float2 s2 = make_float2(step, step), m2 = make_float2(mn, mn);
+    auto put = [&](int r, uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3) {
+        // two values per paired-fp32 op (same IEEE operations as the scalar fma(code + 0.5, step, mn))
+        const float2 h = make_float2(-8388607.5f, -8388607.5f);
+        const float2 lo = __ffma2_rn(__fadd2_rn(make_float2(__uint_as_float(p0), __uint_as_float(p1)), h), s2, m2);
+        const float2 hi = __ffma2_rn(__fadd2_rn(make_float2(__uint_as_float(p2), __uint_as_float(p3)), h), s2, m2);
+        __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch),
+               make_float4(lo.x, lo.y, hi.x, hi.y));
+    };
     if (ib < t.nb) {
+        if (TWO) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int r = r0 + 4 * u;
-            const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
-            // two values per paired-fp32 op (same IEEE operations as the scalar fma(code + 0.5, step, mn))
-            const float2 s2 = make_float2(step, step), m2 = make_float2(mn, mn);
-            const float2 lo = __ffma2_rn(bin_centre2(c.x, c.y), s2, m2), hi = __ffma2_rn(bin_centre2(c.z, c.w), s2, m2);
-            const float4 v = make_float4(lo.x, lo.y, hi.x, hi.y);
-            __stcs(reinterpret_cast<float4 *>(dbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch), v);
+            for (int u = 0; u < 4; ++u) {
+                const int r = r0 + 4 * u;
+                const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
+                put(r, 0x4B000000u | c.x, 0x4B000000u | c.y, 0x4B000000u | c.z, 0x4B000000u | c.w);
+            }
+        } else {
+            // codes j = xi + 4r of rows r = r0 + 4u (u < 2) are the low halves of words 4r + xi, those of
+            // rows r + 8 the high halves of the same words
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int r = r0 + 4 * u;
+                const uint4 c = *reinterpret_cast<const uint4 *>(&cw[ib][4 * r]);
+                put(r, pat_lo(c.x), pat_lo(c.y), pat_lo(c.z), pat_lo(c.w));
+                put(r + 8, pat_hi(c.x), pat_hi(c.y), pat_hi(c.z), pat_hi(c.w));
+            }
         }
     }
 }
@@ -199,30 +235,27 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
                                                int q_rt, uint32_t (*cw)[CODE_LD], int lane) {
     const int q = QT ? QT : q_rt;
     const int ib = lane & 7, r0 = lane >> 3;
-    float mn = v[0].x, mx = v[0].x;
-    // x * 0 is NaN exactly for NaN and Inf: one paired FMA per two values flags them (fminf/fmaxf skip NaNs)
-    float2 nz0 = make_float2(0.f, 0.f), nz1 = nz0;
-    const float2 zero2 = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            mn = fminf(mn, e[c]);
-            mx = fmaxf(mx, e[c]);
-        }
-        nz0 = __ffma2_rn(make_float2(v[u].x, v[u].y), zero2, nz0);
-        nz1 = __ffma2_rn(make_float2(v[u].z, v[u].w), zero2, nz1);
+    // block min / max with NaN propagation (FMNMX3.NAN): 16 values in 8 + 8 ops, and a NaN anywhere in the
+    // block makes both NaN, which the range check below rejects together with +-Inf and |x| >= 2^126
+    const float e[16] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w,
+                         v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
+    // a depth-3 tree (5 + 2 + 1 ops), not an 8-deep chain: the statistics sit on the encoder's critical path
+    float mn, mx;
+    {
+        const float a0 = min3n(e[0], e[1], e[2]), a1 = min3n(e[3], e[4], e[5]), a2 = min3n(e[6], e[7], e[8]),
+                    a3 = min3n(e[9], e[10], e[11]), a4 = min3n(e[12], e[13], e[14]);
+        const float b0 = max3n(e[0], e[1], e[2]), b1 = max3n(e[3], e[4], e[5]), b2 = max3n(e[6], e[7], e[8]),
+                    b3 = max3n(e[9], e[10], e[11]), b4 = max3n(e[12], e[13], e[14]);
+        mn = min2n(min3n(a0, a1, a2), min3n(a3, a4, e[15]));
+        mx = max2n(max3n(b0, b1, b2), max3n(b3, b4, e[15]));
     }
-    const float nzs = __fadd_rn(__fadd_rn(nz0.x, nz0.y), __fadd_rn(nz1.x, nz1.y));
-    const bool nan = nzs != nzs;
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 8));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    mn = min2n(mn, __shfl_xor_sync(0xffffffffu, mn, 8));
+    mx = max2n(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mn = min2n(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
+    mx = max2n(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
     mn = __fadd_rn(mn, 0.0f);  // -0 -> +0
     mx = __fadd_rn(mx, 0.0f);
-    const bool bad = live && (nan || !(fabsf(mn) < 0x1p126f) || !(fabsf(mx) < 0x1p126f));
+    const bool bad = live && (!(fabsf(mn) < 0x1p126f) || !(fabsf(mx) < 0x1p126f));
     const float range = __fsub_rn(mx, mn);
     const float step = __fmul_rn(range, pow2f(-q));
     const bool small = !(step >= 0x1p-126f);
@@ -241,11 +274,27 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
         return TWO ? make_uint2(min(cmax, ba - 0x4B000000u), min(cmax, bb - 0x4B000000u))
                    : make_uint2(min(cmax + 0x4B000000u, ba), min(cmax + 0x4B000000u, bb));
     };
+    if (TWO) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 4 * u;  // r = yi + 4 zi, so j = xi + 4 r
-        const uint2 c01 = code2(v[u].x, v[u].y), c23 = code2(v[u].z, v[u].w);
-        *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) = make_uint4(c01.x, c01.y, c23.x, c23.y);
+        for (int u = 0; u < 4; ++u) {
+            const int r = r0 + 4 * u;  // r = yi + 4 zi, so j = xi + 4 r
+            const uint2 c01 = code2(v[u].x, v[u].y), c23 = code2(v[u].z, v[u].w);
+            *reinterpret_cast<uint4 *>(&cw[ib][4 * r]) = make_uint4(c01.x, c01.y, c23.x, c23.y);
+        }
+    } else {
+        // q <= 16: word m = (code m) | (code m+32) << 16 is the transpose's input row m.  Codes m and
+        // m + 32 are rows r and r + 8 of this lane (u and u + 2), so the packing is in registers
+        uint2 c[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            c[u][0] = code2(v[u].x, v[u].y);
+            c[u][1] = code2(v[u].z, v[u].w);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            *reinterpret_cast<uint4 *>(&cw[ib][4 * (r0 + 4 * u)]) =
+                make_uint4(__byte_perm(c[u][0].x, c[u + 2][0].x, 0x5410), __byte_perm(c[u][0].y, c[u + 2][0].y, 0x5410),
+                           __byte_perm(c[u][1].x, c[u + 2][1].x, 0x5410), __byte_perm(c[u][1].y, c[u + 2][1].y, 0x5410));
     }
     __syncwarp();
     // ---- bit planes: lane m of the transpose owns plane (m & 15), half (m >> 4)
@@ -256,12 +305,15 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     const int wi1 = (TWO && 16 + b < q) ? 2 + 2 * (q - 17 - b) + half : -1;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {  // unconditional (convergent shuffles); stores only for live blocks
-        const uint32_t c_lo = cw[i][lane], c_hi = cw[i][lane + 32];
         uint32_t *rec = rec0 + i * recw;
         const bool st = (live_mask >> i) & 1u;
-        const uint32_t T0 = X((c_lo & 0xFFFFu) | (c_hi << 16));
-        if (st && wi0 >= 0) rec[wi0] = T0;
-        if (TWO) {
+        if (!TWO) {
+            const uint32_t T0 = X(cw[i][lane]);
+            if (st && wi0 >= 0) rec[wi0] = T0;
+        } else {
+            const uint32_t c_lo = cw[i][lane], c_hi = cw[i][lane + 32];
+            const uint32_t T0 = X((c_lo & 0xFFFFu) | (c_hi << 16));
+            if (st && wi0 >= 0) rec[wi0] = T0;
             const uint32_t T1 = X((c_lo >> 16) | ((c_hi >> 16) << 16));
             if (st && wi1 >= 0) rec[wi1] = T1;
         }
@@ -1376,6 +1428,346 @@ __global__ void __launch_bounds__(256) star7_step_kernel(const float *__restrict
         fm = f0;
         f0 = fp;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Two leapfrog steps fused (NEXT-2, SURVEY §8(f) "2-step register blocking"; P:L233 / P:L254 "optimizing
+// GPU computation"), out of place:
+//     C = p(t+1) = step(A = p(t-1), B = p(t))  on planes [z1lo, z1hi)
+//     D = p(t+2) = step(B, C)                  on planes [z2lo, z2hi)
+// per cell-update pair 12 B read (A, B, v) + 8 B written (C, D) = 10 B per update instead of 16.
+// A CTA owns a 64 x 16 tile of D and marches z.  Level t+1 is computed on the tile plus its R halo
+// (72 x 24, "ext"), plane z1 = z + 4 ahead of the level-t+2 plane z: its x/y neighbours come from a TMA
+// ring of B boxes with a 2R halo (80 x 32), its z neighbours from per-thread register queues (own 2 x 2
+// cells and up to two halo pairs per thread); the finished level-t+1 plane goes to a shared ring Q (the
+// x/y neighbours of step 2) and, for the thread's own cells, into a second register queue (step 2's z
+// neighbours).  Ext cells outside the domain or planes outside [z1lo, z1hi) take B's value (Dirichlet:
+// every level holds the initial boundary values).  Every operation is the single-step kernel's
+// (difference form, paired fp32, same order), so the results are bitwise those of two oocs_step calls.
+// C and D are written on interior cells only: their halo (x/y ring, boundary planes) is the caller's.
+// ---------------------------------------------------------------------------
+namespace st2 {
+constexpr int TX = 64, TY = 16, THREADS = 256;
+constexpr int EW = TX + 2 * R, EH = TY + 2 * R;          // ext tile (level t+1), 72 x 24
+constexpr int BW = TX + 4 * R, BH = TY + 4 * R;          // B box, 80 x 32
+constexpr int NS = 9, NB = 3, D = 2;                     // ring slots, A/V stages, prefetch distance
+constexpr int HALO_PAIRS = (EW / 2) * EH - (TX / 2) * TY;  // 352 float2 pairs of ext outside the tile
+constexpr uint32_t BBYTES = BW * BH * 4, EBYTES = EW * EH * 4;
+struct Smem {
+    float b[NS][BH][BW];
+    float q[NS][EH][EW];
+    float a[NB][EH][EW];
+    float v[NB][EH][EW];
+    unsigned long long bar[NB + 1];
+};
+struct Args {
+    const float *A, *B, *V;
+    float *C, *D;
+    int nx, ny, ax, ay, planes;
+    int z1lo, z1hi, z2lo, z2hi, zchunk;
+    int64_t pitch, pstride;
+    float dt;
+};
+// ext coordinates (ex, ey) of halo pair j (row-major over the 4 full rows above and below the tile, then
+// the 16 rows' left / right 4-column strips)
+__device__ __forceinline__ void halo_pair(int j, int &ex, int &ey) {
+    if (j < 8 * (EW / 2)) {
+        const int row = j / (EW / 2);
+        ey = row < R ? row : row + TY;
+        ex = 2 * (j % (EW / 2));
+    } else {
+        const int k = j - 8 * (EW / 2);
+        ey = R + (k >> 2);
+        const int side = k & 3;
+        ex = side < 2 ? 2 * side : TX + R + 2 * (side - 2);
+    }
+}
+}  // namespace st2
+
+// the difference-form Laplacian of one pair row (x neighbours from a box row, y neighbours given, z from
+// a queue) -- the single-step kernel's operation order exactly
+#define ST2_LAP(lap, P, row, col, yl, yh, QZ, r, OFF)                                                        \
+    do {                                                                                                     \
+        const float2 xa = *reinterpret_cast<const float2 *>(&P[row][col]);                                 \
+        const float2 xb = *reinterpret_cast<const float2 *>(&P[row][col + 2]);                             \
+        const float2 xc = *reinterpret_cast<const float2 *>(&P[row][col + 6]);                             \
+        const float2 xd = *reinterpret_cast<const float2 *>(&P[row][col + 8]);                             \
+        const float2 f0 = QZ[((OFF) + 4) % 9] r;                                                             \
+        const float2 f2 = __fadd2_rn(f0, f0);                                                                \
+        const float2 nf2 = make_float2(-f2.x, -f2.y);                                                        \
+        auto d = [&](float2 lo, float2 hi) { return __fadd2_rn(__fadd2_rn(lo, hi), nf2); };                  \
+        lap = __fmul2_rn(k1, d(make_float2(xb.y, f0.x), make_float2(f0.y, xc.x)));                           \
+        lap = __ffma2_rn(k2, d(xb, xc), lap);                                                                \
+        lap = __ffma2_rn(k3, d(make_float2(xa.y, xb.x), make_float2(xc.y, xd.x)), lap);                      \
+        lap = __ffma2_rn(k4, d(xa, xd), lap);                                                                \
+        lap = __ffma2_rn(k1, d(yl[3], yh[5]), lap);                                                          \
+        lap = __ffma2_rn(k2, d(yl[2], yh[6]), lap);                                                          \
+        lap = __ffma2_rn(k3, d(yl[1], yh[7]), lap);                                                          \
+        lap = __ffma2_rn(k4, d(yl[0], yh[8]), lap);                                                          \
+        lap = __ffma2_rn(k1, d(QZ[((OFF) + 3) % 9] r, QZ[((OFF) + 5) % 9] r), lap);                          \
+        lap = __ffma2_rn(k2, d(QZ[((OFF) + 2) % 9] r, QZ[((OFF) + 6) % 9] r), lap);                          \
+        lap = __ffma2_rn(k3, d(QZ[((OFF) + 1) % 9] r, QZ[((OFF) + 7) % 9] r), lap);                          \
+        lap = __ffma2_rn(k4, d(QZ[((OFF) + 0) % 9] r, QZ[((OFF) + 8) % 9] r), lap);                          \
+    } while (0)
+
+__device__ __forceinline__ float2 st2_update(float2 lap, float2 f0, float2 pv, float2 vv, float dt) {
+    const float2 f2 = __fadd2_rn(f0, f0);
+    const float2 vd = __fmul2_rn(vv, make_float2(dt, dt));
+    return __ffma2_rn(__fmul2_rn(vd, vd), lap, __fadd2_rn(f2, make_float2(-pv.x, -pv.y)));
+}
+
+template <int OFF>
+__device__ __forceinline__ bool st2_plane(st2::Smem &S, const CUtensorMap *mB, const CUtensorMap *mA,
+                                          const CUtensorMap *mV, const st2::Args &a, int z1, int zs1, int ze1,
+                                          int zs2, int ze2, int x0, int y0, float2 (&q)[9][2], float2 (&g)[9][2],
+                                          float2 (&h)[2][9], uint32_t &ph, int hx0, int hy0, int hx1, int hy1,
+                                          bool hv0, bool hv1) {
+    using namespace st2;
+    if (z1 >= ze1) return false;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();  // plane z1-1 is done everywhere: its ring slots may be refilled
+    if (tid == 0 && z1 + D < ze1) {
+        constexpr int ps = (OFF + 4 + D + R) % NS, st = (OFF + D) % NB;
+        unsigned long long *bar = &S.bar[st];
+        mbar_expect_tx(bar, BBYTES + 2 * EBYTES);
+        tma_load_3d(&S.b[ps][0][0], mB, XOFF - R + x0, y0 - R, z1 + D + R, bar);
+        tma_load_3d(&S.a[st][0][0], mA, XOFF + x0, y0, z1 + D, bar);
+        tma_load_3d(&S.v[st][0][0], mV, XOFF + x0, y0, z1 + D, bar);
+    }
+    constexpr int st = OFF % NB, sz = (OFF + 4) % NS, sz4 = (OFF + 8) % NS;
+    mbar_wait(&S.bar[st], (ph >> st) & 1u);
+    ph ^= 1u << st;
+    const float2 k1 = make_float2(C1, C1), k2 = make_float2(C2, C2), k3 = make_float2(C3, C3),
+                 k4 = make_float2(C4, C4);
+    const bool in1 = z1 >= a.z1lo && z1 < a.z1hi;
+    const float(*P)[BW] = S.b[sz];
+    const int cx = 2 * lane, cy = 2 * warp;
+    // ---- step 1, own 2 x 2 cells (box (cx+8, cy+8)): feed the queue with plane z1+4
+    q[(OFF + 8) % 9][0] = *reinterpret_cast<const float2 *>(&S.b[sz4][2 * R + cy][2 * R + cx]);
+    q[(OFF + 8) % 9][1] = *reinterpret_cast<const float2 *>(&S.b[sz4][2 * R + cy + 1][2 * R + cx]);
+    {
+        float2 yr[10];
+#pragma unroll
+        for (int m = 0; m < 10; ++m)
+            if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&P[R + cy + m][2 * R + cx]);
+        yr[4] = q[(OFF + 4) % 9][0];
+        yr[5] = q[(OFF + 4) % 9][1];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            float2 lap;
+            ST2_LAP(lap, P, 2 * R + cy + r, R + cx, (yr + r), (yr + r), q, [r], OFF);
+            const float2 pv = *reinterpret_cast<const float2 *>(&S.a[st][R + cy + r][R + cx]);
+            const float2 vv = *reinterpret_cast<const float2 *>(&S.v[st][R + cy + r][R + cx]);
+            const float2 f0 = q[(OFF + 4) % 9][r];
+            const int x = x0 + cx, y = y0 + cy + r;
+            float2 o = st2_update(lap, f0, pv, vv, a.dt);
+            // out of the domain (the R-cell halo and beyond) or outside [z1lo, z1hi): B's value
+            if (!in1 || y >= a.ny) o = f0;
+            else if (x + 1 >= a.nx) o = make_float2(x < a.nx ? o.x : f0.x, f0.y);
+            g[(OFF + 8) % 9][r] = o;
+            *reinterpret_cast<float2 *>(&S.q[OFF % NS][R + cy + r][R + cx]) = o;
+            if (in1 && z1 >= a.z1lo && y < a.ny && x < a.nx) {
+                // C: own cells of the planes this CTA is responsible for
+                const bool mine = (z1 >= zs2 || zs2 == a.z2lo) && (z1 < ze2 || ze2 == a.z2hi);
+                if (mine) {
+                    float *dst = a.C + (int64_t)z1 * a.pstride + (int64_t)(y + R) * a.pitch + x + R + XOFF;
+                    if (x + 1 < a.nx) __stcs(reinterpret_cast<float2 *>(dst), o);
+                    else *dst = o.x;
+                }
+            }
+        }
+    }
+    // ---- step 1, halo pairs: one row each
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const bool hv = j ? hv1 : hv0;
+        const int ex = j ? hx1 : hx0, ey = j ? hy1 : hy0;
+        if (!hv) continue;
+        h[j][(OFF + 8) % 9] = *reinterpret_cast<const float2 *>(&S.b[sz4][R + ey][R + ex]);
+        float2 yv[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m)
+            if (m != 4) yv[m] = *reinterpret_cast<const float2 *>(&P[ey + m][R + ex]);
+        const float2 f0 = h[j][(OFF + 4) % 9];
+        float2 lap;
+        {
+            const float2 xa = *reinterpret_cast<const float2 *>(&P[R + ey][ex]);
+            const float2 xb = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 2]);
+            const float2 xc = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 6]);
+            const float2 xd = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 8]);
+            const float2 f2 = __fadd2_rn(f0, f0);
+            const float2 nf2 = make_float2(-f2.x, -f2.y);
+            auto d = [&](float2 lo, float2 hi) { return __fadd2_rn(__fadd2_rn(lo, hi), nf2); };
+            lap = __fmul2_rn(k1, d(make_float2(xb.y, f0.x), make_float2(f0.y, xc.x)));
+            lap = __ffma2_rn(k2, d(xb, xc), lap);
+            lap = __ffma2_rn(k3, d(make_float2(xa.y, xb.x), make_float2(xc.y, xd.x)), lap);
+            lap = __ffma2_rn(k4, d(xa, xd), lap);
+            lap = __ffma2_rn(k1, d(yv[3], yv[5]), lap);
+            lap = __ffma2_rn(k2, d(yv[2], yv[6]), lap);
+            lap = __ffma2_rn(k3, d(yv[1], yv[7]), lap);
+            lap = __ffma2_rn(k4, d(yv[0], yv[8]), lap);
+            lap = __ffma2_rn(k1, d(h[j][(OFF + 3) % 9], h[j][(OFF + 5) % 9]), lap);
+            lap = __ffma2_rn(k2, d(h[j][(OFF + 2) % 9], h[j][(OFF + 6) % 9]), lap);
+            lap = __ffma2_rn(k3, d(h[j][(OFF + 1) % 9], h[j][(OFF + 7) % 9]), lap);
+            lap = __ffma2_rn(k4, d(h[j][(OFF + 0) % 9], h[j][(OFF + 8) % 9]), lap);
+        }
+        const float2 pv = *reinterpret_cast<const float2 *>(&S.a[st][ey][ex]);
+        const float2 vv = *reinterpret_cast<const float2 *>(&S.v[st][ey][ex]);
+        float2 o = st2_update(lap, f0, pv, vv, a.dt);
+        const int x = x0 + ex - R, y = y0 + ey - R;
+        const bool yin = y >= 0 && y < a.ny;
+        const bool x0in = x >= 0 && x < a.nx, x1in = x + 1 >= 0 && x + 1 < a.nx;
+        if (!in1 || !yin) o = f0;
+        else o = make_float2(x0in ? o.x : f0.x, x1in ? o.y : f0.y);
+        *reinterpret_cast<float2 *>(&S.q[OFF % NS][ey][ex]) = o;
+    }
+    // ---- step 2 at plane z = z1 - 4: x/y neighbours from Q plane z (written 4 iterations ago), z from g
+    const int z = z1 - R;
+    if (z >= zs2 && z < ze2) {
+        const float(*Q)[EW] = S.q[(OFF + 5) % NS];
+        float2 yr[10];
+#pragma unroll
+        for (int m = 0; m < 10; ++m)
+            if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&Q[cy + m][R + cx]);
+        yr[4] = g[(OFF + 4) % 9][0];
+        yr[5] = g[(OFF + 4) % 9][1];
+        const int x = x0 + cx;
+        const int64_t g0 = (int64_t)(y0 + cy + R) * a.pitch + x + R + XOFF;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int y = y0 + cy + r;
+            if (y >= a.ny || x >= a.nx) continue;
+            float2 lap;
+            ST2_LAP(lap, Q, R + cy + r, cx, (yr + r), (yr + r), g, [r], OFF);
+            const float *vp = a.V + (int64_t)z * a.pstride + g0 + r * a.pitch;
+            const float2 vv = x + 1 < a.nx ? __ldg(reinterpret_cast<const float2 *>(vp)) : make_float2(__ldg(vp), 0.f);
+            const float2 o = st2_update(lap, g[(OFF + 4) % 9][r], q[OFF % 9][r], vv, a.dt);
+            float *dst = a.D + (int64_t)z * a.pstride + g0 + r * a.pitch;
+            if (x + 1 < a.nx) __stcs(reinterpret_cast<float2 *>(dst), o);
+            else *dst = o.x;
+        }
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(st2::THREADS, 1)
+stencil_step2_kernel(const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mA,
+                     const __grid_constant__ CUtensorMap mV, const st2::Args a) {
+    using namespace st2;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zs2 = a.z2lo + blockIdx.z * a.zchunk, ze2 = min(a.z2hi, zs2 + a.zchunk);
+    if (zs2 >= ze2) return;
+    const int zs1 = zs2 - R, ze1 = ze2 + R;  // level t+1 planes this CTA computes (B's copy outside [z1lo, z1hi))
+    if (tid == 0) {
+        for (int i = 0; i <= NB; ++i) mbar_init(&S.bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long *pro = &S.bar[NB];
+        mbar_expect_tx(pro, 4 * BBYTES);
+        for (int i = 0; i < 4; ++i) tma_load_3d(&S.b[(4 + i) % NS][0][0], &mB, XOFF - R + x0, y0 - R, zs1 + i, pro);
+        for (int j = 0; j < D; ++j) {
+            unsigned long long *bar = &S.bar[j % NB];
+            mbar_expect_tx(bar, BBYTES + 2 * EBYTES);
+            tma_load_3d(&S.b[(j + 4 + R) % NS][0][0], &mB, XOFF - R + x0, y0 - R, zs1 + j + R, bar);
+            tma_load_3d(&S.a[j % NB][0][0], &mA, XOFF + x0, y0, zs1 + j, bar);
+            tma_load_3d(&S.v[j % NB][0][0], &mV, XOFF + x0, y0, zs1 + j, bar);
+        }
+    }
+    // halo pairs of this thread, and the register queues of B (planes zs1-4 .. zs1+3) from global memory;
+    // cells outside the allocated grid or planes outside the buffer read as 0 (never used for a result)
+    int hx0 = 0, hy0 = 0, hx1 = 0, hy1 = 0;
+    const bool hv0 = tid < HALO_PAIRS, hv1 = tid + THREADS < HALO_PAIRS;
+    if (hv0) halo_pair(tid, hx0, hy0);
+    if (hv1) halo_pair(tid + THREADS, hx1, hy1);
+    auto ldq = [&](int ex, int ey, int z) -> float2 {
+        // ext (ex, ey) -> allocated column x0 + ex (interior x0 + ex - R), row y0 + ey
+        const int ac = x0 + ex, ar = y0 + ey;
+        if (z < 0 || z >= a.planes || ar < 0 || ar >= a.ay || ac < 0 || ac + 1 >= a.ax + 1) return make_float2(0.f, 0.f);
+        const float *p = a.B + (int64_t)z * a.pstride + (int64_t)ar * a.pitch + XOFF + ac;
+        return ac + 1 < a.ax ? __ldg(reinterpret_cast<const float2 *>(p)) : make_float2(__ldg(p), 0.f);
+    };
+    float2 q[9][2], g[9][2], h[2][9];
+    const int cx = 2 * lane, cy = 2 * warp;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int z = zs1 - R + m;
+        q[m][0] = ldq(R + cx, R + cy, z);
+        q[m][1] = ldq(R + cx, R + cy + 1, z);
+        h[0][m] = hv0 ? ldq(hx0, hy0, z) : make_float2(0.f, 0.f);
+        h[1][m] = hv1 ? ldq(hx1, hy1, z) : make_float2(0.f, 0.f);
+        g[m][0] = g[m][1] = make_float2(0.f, 0.f);
+    }
+    q[8][0] = q[8][1] = h[0][8] = h[1][8] = g[8][0] = g[8][1] = make_float2(0.f, 0.f);
+    mbar_wait(&S.bar[NB], 0);
+    uint32_t ph = 0;
+    for (int zb = zs1; zb < ze1; zb += 9) {
+#define ST2P(O)                                                                                                 \
+    if (!st2_plane<O>(S, &mB, &mA, &mV, a, zb + O, zs1, ze1, zs2, ze2, x0, y0, q, g, h, ph, hx0, hy0, hx1, hy1, \
+                      hv0, hv1))                                                                               \
+        break;
+        ST2P(0) ST2P(1) ST2P(2) ST2P(3) ST2P(4) ST2P(5) ST2P(6) ST2P(7) ST2P(8)
+#undef ST2P
+    }
+}
+#undef ST2_LAP
+
+cudaError_t launch_step2(const float *vel, const float *A, const float *B, float *C, float *Dd, int64_t ax, int64_t ay,
+                         int64_t pitch, int64_t planes, int64_t z1lo, int64_t z1hi, int64_t z2lo, int64_t z2hi,
+                         float dt, cudaStream_t st) {
+    using namespace st2;
+    if (z2hi <= z2lo) return cudaSuccess;
+    // step 1 must cover what step 2 reads: [z2lo - R, z2hi + R) within [z1lo, z1hi) except Dirichlet planes
+    if (z1lo > z2lo || z1hi < z2hi || z2lo - z1lo > R || z1hi - z2hi > R || z1lo < R || z1hi > planes - R)
+        return cudaErrorInvalidValue;
+    const size_t smem = sizeof(Smem);
+    cudaError_t e = cudaFuncSetAttribute(stencil_step2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mB, mA, mV;
+    if (!make_map(&mB, B, pitch, ay, planes, BW, BH) || !make_map(&mA, A, pitch, ay, planes, EW, EH) ||
+        !make_map(&mV, vel, pitch, ay, planes, EW, EH))
+        return cudaErrorInvalidValue;
+    Args a{};
+    a.A = A;
+    a.B = B;
+    a.V = vel;
+    a.C = C;
+    a.D = Dd;
+    a.nx = (int)(ax - 2 * R);
+    a.ny = (int)(ay - 2 * R);
+    a.ax = (int)ax;
+    a.ay = (int)ay;
+    a.planes = (int)planes;
+    a.z1lo = (int)z1lo;
+    a.z1hi = (int)z1hi;
+    a.z2lo = (int)z2lo;
+    a.z2hi = (int)z2hi;
+    a.pitch = pitch;
+    a.pstride = ay * pitch;
+    a.dt = dt;
+    const int gx = (a.nx + TX - 1) / TX, gy = (a.ny + TY - 1) / TY;
+    const int Z = (int)(z2hi - z2lo), tiles = gx * gy;
+    // z split: whole waves of 148 CTAs (1 per SM), each extra split costs 2R redundant level-(t+1) planes
+    int best = 1;
+    double best_eff = 0;
+    for (int nzc = 1; nzc <= 16; ++nzc) {
+        const int chunk = (Z + nzc - 1) / nzc;
+        if (nzc > 1 && chunk < 24) break;
+        const double waves = (double)tiles * ((Z + chunk - 1) / chunk) / 148.0;
+        const double eff = waves / std::ceil(waves) * (double)chunk / (chunk + 2.0 * R + 4.0);
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = nzc;
+        }
+    }
+    a.zchunk = (Z + best - 1) / best;
+    const dim3 grid(gx, gy, (Z + a.zchunk - 1) / a.zchunk);
+    stencil_step2_kernel<<<grid, THREADS, smem, st>>>(mB, mA, mV, a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,

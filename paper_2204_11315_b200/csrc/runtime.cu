@@ -1624,6 +1624,19 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
     return OOCS_OK;
 }
 
+oocs_status oocs_step2(const float *vel, const float *A, const float *B, float *C, float *D, int64_t ax, int64_t ay,
+                       int64_t planes, int64_t pitch, float dt, int64_t z1_lo, int64_t z1_hi, int64_t z2_lo,
+                       int64_t z2_hi, void *stream) {
+    if (ax % 4 || ay % 4 || pitch < ax + XOFF || pitch % 32 || z1_lo < R || z1_hi > planes - R || z1_lo > z2_lo ||
+        z2_lo - z1_lo > R || z2_hi > z1_hi || z1_hi - z2_hi > R || z2_lo > z2_hi || !A || !B || !C || !D || !vel ||
+        C == A || C == B || D == A || D == B || C == D) {
+        set_error("oocs_step2: bad geometry, plane ranges or aliasing");
+        return OOCS_ERR_CONFIG;
+    }
+    CU(launch_step2(vel, A, B, C, D, ax, ay, pitch, planes, z1_lo, z1_hi, z2_lo, z2_hi, dt, (cudaStream_t)stream));
+    return OOCS_OK;
+}
+
 const char *oocs_last_error(void) { return g_last_error.c_str(); }
 int32_t oocs_abi_version(void) { return OOCS_ABI_VERSION; }
 
