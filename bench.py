@@ -72,8 +72,6 @@ def parse():
     ap.add_argument("--no-error", action="store_true", help="skip the in-core error run")
     ap.add_argument("--no-device-resident", action="store_true", help="skip the HBM-resident variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fuse-encode", action="store_true", help="fuse each chunk's last step with its encode "
-                    "(device store, BlockQuant; OOCS_FLAG_FUSE_ENCODE)")
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
     ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp", "trunc16"],
                     help="fixed-rate codec of the compressed state (ZFP = NEXT-1)")
@@ -375,18 +373,21 @@ def main():
         rate = 16  # bfloat16
     import torch
 
-    nz = nzr * world
-    nblocks = nbr * world
-    workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps "
-                f"per step, temporal depth k={k}, {CODEC_NAME[args.codec]} rate {rate} bits/value, single "
-                f"working buffer, compressed state in pinned host memory (out-of-core, PCIe in the timed region)")
-    raw_gb = 3 * (nx + 2 * R) * (ny + 2 * R) * (nzr + 2 * R) * 4 / 1e9
-    config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
-              "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
-              "store": "pinned host", "raw_state_gb_per_gpu": raw_gb,
-              "parallelism": f"z-slabs x{world}",
-              "l2": f"inputs larger than L2 (compressed state {3 * nx * ny * nzr * rate / 8 / 1e9:.1f} GB/GPU "
-                    ">> 126 MB, streamed over PCIe every step), no flush needed"}
+    def describe(nzr, nbr):
+        nz, nblocks = nzr * world, nbr * world
+        workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps "
+                    f"per step, temporal depth k={k}, {CODEC_NAME[args.codec]} rate {rate} bits/value, single "
+                    f"working buffer, compressed state in pinned host memory (out-of-core, PCIe in the timed region)")
+        raw_gb = 3 * (nx + 2 * R) * (ny + 2 * R) * (nzr + 2 * R) * 4 / 1e9
+        config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
+                  "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
+                  "store": "pinned host", "raw_state_gb_per_gpu": raw_gb,
+                  "parallelism": f"z-slabs x{world}",
+                  "l2": f"inputs larger than L2 (compressed state {3 * nx * ny * nzr * rate / 8 / 1e9:.1f} GB/GPU "
+                        ">> 126 MB, streamed over PCIe every step), no flush needed"}
+        return nz, nblocks, config
+
+    nz, nblocks, config = describe(nzr, nbr)
 
     if args.impl == "reference":
         if rank != 0:
@@ -455,7 +456,7 @@ def main():
                              rate_bits=rate if codec != "identity" else 32, mode=mode, store=store, device=local,
                              rank=rank if wl is None else 0, world=world if wl is None else 1,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
-                             fusion=args.fuse_encode, decoded_velocity=decoded_velocity)
+                             decoded_velocity=decoded_velocity)
         pl = oocs.Plan(c)
         if world > 1 and wl is None:
             odist.connect(pl, gloo=gloo)
@@ -469,6 +470,22 @@ def main():
         store="host", device=local, rank=rank, world=world))
     avail = host_mem_available()
     local_ranks = env_int("LOCAL_WORLD_SIZE", world)
+    if avail is not None and est.store_bytes * local_ranks > 0.8 * avail and nbr > 1:
+        # weak scaling on a node whose host RAM cannot pin every rank's full slab: fewer chunks of the same
+        # width per rank (the per-chunk work, k, r and T unchanged), said so in the config
+        fit = int(nbr * 0.8 * avail / (est.store_bytes * local_ranks))
+        if fit >= 1:
+            full = (nzr, nbr)
+            nzr, nbr = nzr // nbr * fit, fit
+            nz, nblocks, config = describe(nzr, nbr)
+            config["host_ram_limited"] = {"per_rank_full": {"nz": full[0], "chunks": full[1]},
+                                          "per_rank_run": {"nz": nzr, "chunks": nbr},
+                                          "host_mem_available_gb": avail / 1e9, "local_ranks": local_ranks}
+            print(f"bench: host RAM fits {fit} of {full[1]} chunks per rank; running {nzr} planes per rank",
+                  file=sys.stderr)
+            est = oocs.oocs_plan_estimate(oocs.make_config(
+                nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=args.codec, rate_bits=rate,
+                mode="swb", store="host", device=local, rank=rank, world=world))
     if avail is not None and est.store_bytes * local_ranks > 0.9 * avail:
         print(f"bench: the pinned host stores need {est.store_bytes * local_ranks / 1e9:.1f} GB, the host has "
               f"{avail / 1e9:.1f} GB available", file=sys.stderr)

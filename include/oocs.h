@@ -116,11 +116,8 @@ typedef enum {
  * P:L244) resident in HBM instead of re-sending it every sweep (SPEC S:L508's config flag);
  * H2D then moves the two pressure arrays only.  Off by default (paper-faithful accounting). */
 #define OOCS_FLAG_RESIDENT_VELOCITY 2u
-/* Device store + BlockQuant: fuse every chunk's last step with the encode of its owned planes (level
- * k is never written back; the two time levels go straight into S_{t+1}).  Off by default: it moves
- * 35% fewer HBM bytes than step + encode but is issue-bound and measures ~1.5%
- * slower on B200.  Ignored by other modes. */
-#define OOCS_FLAG_FUSE_ENCODE 4u
+/* Flag value 4 is retired (ABI 1's OOCS_FLAG_FUSE_ENCODE, the last step fused with the encode: measured
+ * slower than step + encode on B200 and removed in ABI 2); it is rejected. */
 /* Record a CUDA-event span around every work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, SEND) of a
  * run; read it back with oocs_timeline (the analog of the paper's pipeline figures fig:pipe1 /
  * fig:newbot).  Costs two event records per op. */
@@ -400,20 +397,6 @@ oocs_status oocs_encode(const float *src, void *dst, int64_t ax, int64_t ay, int
 oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int64_t ax, int64_t ay,
                       int64_t planes, int64_t pitch, float dt, int64_t z_lo, int64_t z_hi,
                       int32_t stencil, void *stream);
-
-/* Two leapfrog steps of the 25-point stencil fused in one pass (NEXT-2 temporal register blocking; the
- * paper's future work "optimizing GPU computation"), OUT of place:
- *   C <- p(t+1) = 2 B - A + (v dt)^2 Lap25(B)   on buffer planes [z1_lo, z1_hi)
- *   D <- p(t+2) = 2 C - B + (v dt)^2 Lap25(C)   on buffer planes [z2_lo, z2_hi)
- * with A = p(t-1), B = p(t), interior x, y; bitwise equal to two oocs_step calls.  HBM per update pair:
- * read A, B, v, write C, D (10 B per cell-update vs 16).  Requires R <= z1_lo <= z2_lo <= z1_lo + R and
- * z2_hi <= z1_hi <= z2_hi + R, z1_hi <= planes - R; level t+1 outside [z1_lo, z1_hi) (in step 2's
- * reach) is taken from B (a Dirichlet boundary plane).  C and D are written on interior cells only:
- * their x/y halo and boundary planes are the caller's (the same values as B's for a Dirichlet run).
- * All pointers DEVICE, working-buffer layout, A/B/V distinct from C/D.  Errors: OOCS_ERR_CONFIG. */
-oocs_status oocs_step2(const float *vel, const float *A, const float *B, float *C, float *D, int64_t ax, int64_t ay,
-                       int64_t planes, int64_t pitch, float dt, int64_t z1_lo, int64_t z1_hi, int64_t z2_lo,
-                       int64_t z2_hi, void *stream);
 
 /* ---- misc -------------------------------------------------------------- */
 const char *oocs_last_error(void);

@@ -22,7 +22,7 @@ __all__ = [
     "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
     "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
     "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_load_device", "oocs_store_device", "oocs_store_read_raw",
-    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step", "oocs_step2",
+    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
     "oocs_peer_handle", "oocs_peer_connect", "PEER_HANDLE_BYTES", "Plan", "XOFF", "pitch_for",
 ]
 
@@ -41,7 +41,6 @@ SCHED = {"alg1": 0, "dag": 1, "dag_func": 2}
 STENCIL = {"acoustic25": 0, "star7": 1}
 FLAG_PROFILE = 1
 FLAG_RESIDENT_VELOCITY = 2
-FLAG_FUSE_ENCODE = 4
 FLAG_TIMELINE = 8
 FLAG_LANE_SINGLE_STREAM = 16
 FLAG_LANE_SPLIT_STREAMS = 32
@@ -141,7 +140,6 @@ def lib():
             "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
             "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
             "oocs_step": ([vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, i32, vp], i32),
-            "oocs_step2": ([vp, vp, vp, vp, vp, i64, i64, i64, i64, f32, i64, i64, i64, i64, vp], i32),
             "oocs_last_error": ([], ctypes.c_char_p),
             "oocs_abi_version": ([], i32),
             "oocs_abi_sizes": ([vp], None),
@@ -161,7 +159,7 @@ def _check(st: int, where: str):
 
 def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bits=16, mode="swb",
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
-                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1", fusion=False,
+                device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1",
                 timeline=False, executor="dispatch", decoded_velocity=False, stencil="acoustic25", v_max=0.0,
                 ext_streams=()) -> Config:
     """ext_streams: up to 8 integer cudaStream_t handles (e.g. torch.cuda.Stream().cuda_stream), lane order."""
@@ -180,7 +178,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.device, c.rank, c.world = device, rank, world
     c.flags = ((FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
                | (FLAG_TIMELINE if timeline else 0) | EXECUTOR[executor]
-               | (FLAG_FUSE_ENCODE if fusion else 0) | (FLAG_DECODED_VELOCITY if decoded_velocity else 0))
+               | (FLAG_DECODED_VELOCITY if decoded_velocity else 0))
     c.device_capacity = device_capacity
     c.stencil = STENCIL[stencil] if isinstance(stencil, str) else stencil
     c.v_max = float(v_max)
@@ -326,12 +324,6 @@ def oocs_step(vel_ptr: int, pprev_ptr: int, pcurr_ptr: int, ax, ay, planes, pitc
     st = STENCIL[stencil] if isinstance(stencil, str) else stencil
     _check(lib().oocs_step(vel_ptr, pprev_ptr, pcurr_ptr, ax, ay, planes, pitch, float(dt), z_lo, z_hi, st,
                            stream or None), "oocs_step")
-
-
-def oocs_step2(vel_ptr: int, a_ptr: int, b_ptr: int, c_ptr: int, d_ptr: int, ax, ay, planes, pitch, dt, z1_lo, z1_hi,
-               z2_lo, z2_hi, stream=0):
-    _check(lib().oocs_step2(vel_ptr, a_ptr, b_ptr, c_ptr, d_ptr, ax, ay, planes, pitch, float(dt), z1_lo, z1_hi, z2_lo,
-                            z2_hi, stream or None), "oocs_step2")
 
 
 @dataclass

@@ -226,8 +226,7 @@ bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
 // Statistics and quantisation are vectorised over the warp's 8 blocks
 // (lane l: block l & 7, 4 rows); the bit planes are then packed per block.
 // ---------------------------------------------------------------------------
-// The per-warp encode core, shared by the standalone encode and the fused last-step kernel: the
-// lane holds 4 rows (r0 + 4u, r = yi + 4 zi) of block ib (v), `live` says whether that block is
+// The per-warp encode core: the lane holds 4 rows (r0 + 4u, r = yi + 4 zi) of block ib (v), `live` says whether that block is
 // written, bit i of live_mask whether block i is.  rec0 = the first block's record (32-bit words),
 // cw = this warp's 8 x CODE_LD code scratch.  Returns true if a live value was rejected.
 template <bool TWO, int QT>
@@ -324,28 +323,16 @@ __device__ __forceinline__ bool bq_encode_core(const float4 (&v)[4], bool live, 
     return bad;
 }
 
-// edge: 0 = every block; 1 = only the x-boundary blocks bx = 0 / nbx-1 (grid.x = 2); 2 = only the
-// y-boundary block rows by = 0 / nby-1 (grid.y = 1, warps 0/1).  Edge modes encode the halo blocks
-// the fused last-step kernel does not produce; they hold the fixed Dirichlet values, identical in
-// every time level, so any array of the working set is a valid source.
 template <bool TWO, int QT>
 __global__ void __launch_bounds__(CODEC_WARPS * 32)
-bq_encode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t pstride, int q_rt, int *err,
-                 int edge) {
+bq_encode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t pstride, int q_rt, int *err) {
     const int q = QT ? QT : q_rt;
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int arr = blockIdx.z / A.slabs;
     const float *__restrict__ src = static_cast<const float *>(A.in(arr));
     uint8_t *__restrict__ dst = static_cast<uint8_t *>(A.out(arr));
-    LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
-    if (edge == 1) {
-        t.b0 = blockIdx.x ? nbx - 1 : 0;
-        t.nb = 1;
-    } else if (edge == 2) {
-        if (warp >= 2) return;
-        t.by = warp ? nby - 1 : 0;
-    }
+    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
     if (t.by >= nby) return;
     // ---- load straight into the statistics layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12
     //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging)
@@ -492,10 +479,9 @@ static unsigned tr16_grid(K kernel, uint64_t n8) {
 // queue indexed at compile time (the plane loop is unrolled by 9), x/y
 // neighbours come from the ring with 64-bit shared loads.
 // ---------------------------------------------------------------------------
-// TY = tile rows (16: 256 threads, 2 CTAs per SM).  The p_curr ring needs 7 slots: at plane z it holds
-// the x/y-neighbour plane z, the queue-feed plane z+4 and the two planes in flight (z+5, z+6).  The
-// plain step uses 9, one per unrolled plane, so every slot index is a compile-time constant; the
-// encoding variant, whose slab staging needs the shared memory, uses 7 with runtime slots.
+// TY = tile rows (16: 256 threads, 2 CTAs per SM).  The p_curr ring has 9 slots, one per unrolled plane
+// (so every slot index is a compile-time constant): at plane z it holds the x/y-neighbour plane z, the
+// queue-feed plane z+4 and the two planes in flight (z+5, z+6).
 template <int TY>
 struct S2T {
     static constexpr int TX = 64, THREADS = 16 * TY, CTAS = TY == 16 ? 2 : 1;
@@ -503,22 +489,13 @@ struct S2T {
     static constexpr int NB = 3, D = 2;                     // p_prev/v stages, prefetch distance
     static constexpr uint32_t PBYTES = PW * PH * 4, TBYTES = TX * TY * 4;
 };
-// ENC selects the stencil variant: 0 = plain step; otherwise the last step of a sweep that also
-// encodes its owned slabs, with one BlockQuant encoder compiled in (q = 15 specialised, generic
-// one-word q <= 16, generic two-word q > 16), keeping the kernel's instruction footprint small
-enum { ENC_NONE = 0, ENC_Q15 = 1, ENC_ONE = 2, ENC_TWO = 3 };
+constexpr int S2_NS = 9;
 
-template <int ENC>
-__host__ __device__ constexpr int s2_ring() { return ENC ? 7 : 9; }
-
-template <int TY, int ENC>
+template <int TY>
 struct S2Smem {
-    float p[s2_ring<ENC>()][TY + 2 * R][64 + 2 * R];
+    float p[S2_NS][TY + 2 * R][64 + 2 * R];
     float pp[3][TY][64];
     float v[3][TY][64];
-    // ENC: the 4-plane slab being completed, [prev/curr][plane][row][col]; the encode phase reuses it
-    // as the warps' code scratch
-    float stage[ENC ? 2 : 1][ENC ? 4 : 1][ENC ? TY : 1][ENC ? 64 : 4];
     unsigned long long bar[4];
 };
 constexpr int S2_TX = 64, S2_NB = 3, S2_D = 2;
@@ -564,29 +541,21 @@ struct StepArgs {
     int nx, ny, z_lo, z_hi, zchunk, gx;
     int64_t pitch, pstride;
     float dt;
-    // ENC only: records of the owned slabs [z_lo, z_hi) of (prev = level k-1, curr = level k)
-    uint32_t *out[2];
-    int nbx, nby, q;
-    int *err;
 };
 
-template <int TY, int ENC>
-__device__ __noinline__ void s2_encode_slab(S2Smem<TY, ENC> &S, const StepArgs &a, int x0, int y0, int zslab);
-
 // one plane of the march; OFF = (z - zs) mod 9 is a compile-time register-queue rotation
-template <int OFF, int TY, int ENC>
-__device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *mP, const CUtensorMap *mPP,
+template <int OFF, int TY>
+__device__ __forceinline__ bool s2_plane(S2Smem<TY> &S, const CUtensorMap *mP, const CUtensorMap *mPP,
                                          const CUtensorMap *mV, const StepArgs &a, int z, int zs, int ze,
                                          int x0, int y0, float2 (&q)[9][2], uint32_t &ph, bool okr0,
                                          bool okr1, int64_t g0) {
     if (z >= ze) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // every thread is done with plane z-1: its ring slots may be refilled
-    // ring slot of plane P is (P - zs + 4) mod NS (NS = 9: OFF + 4 mod 9, known at compile time)
-    constexpr int NS = s2_ring<ENC>();
-    const int rel = NS == 9 ? OFF : z - zs;
+    // ring slot of plane P is (P - zs + 4) mod 9 (OFF + 4 mod 9, known at compile time)
+    constexpr int NS = S2_NS;
     if (tid == 0 && z + S2_D < ze) {
-        const int ps = (rel + 4 + S2_D + R) % NS;  // slot of plane z+D+4 (previously plane z+D+4-NS)
+        constexpr int ps = (OFF + 4 + S2_D + R) % NS;  // slot of plane z+D+4 (previously plane z+D+4-NS)
         constexpr int st = (OFF + S2_D) % S2_NB;     // stage of plane z+D
         unsigned long long *bar = &S.bar[st];
         mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
@@ -597,7 +566,7 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *
     constexpr int st = OFF % S2_NB;
     mbar_wait(&S.bar[st], (ph >> st) & 1u);
     ph ^= 1u << st;
-    const int sz = (rel + 4) % NS, sz4 = (rel + 4 + R) % NS;
+    constexpr int sz = (OFF + 4) % NS, sz4 = (OFF + 4 + R) % NS;
     const int cx = 2 * lane, cy = 2 * warp;
     // feed the queue with plane z+4 (own cells)
     q[(OFF + 8) % 9][0] = *reinterpret_cast<const float2 *>(&S.p[sz4][R + cy][R + cx]);
@@ -650,78 +619,18 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY, ENC> &S, const CUtensorMap *
         const float2 vd = __fmul2_rn(vv, make_float2(a.dt, a.dt));
         out[r] = __ffma2_rn(__fmul2_rn(vd, vd), lap, __fadd2_rn(f2, make_float2(-pv.x, -pv.y)));
     }
-    if (!ENC) {
-        float *dst = a.pprev + (int64_t)z * a.pstride + g0;
-        if (okr0) __stcs(reinterpret_cast<float2 *>(dst), out[0]);
-        if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), out[1]);
-    } else {
-        // last step: level k is not written back; (level k-1, level k) of the own cells go to the
-        // slab staging, and a completed 4-plane slab is encoded straight into the records
-        const int sl = (z - zs) & 3;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            *reinterpret_cast<float2 *>(&S.stage[0][sl][cy + r][cx]) = q[(OFF + 4) % 9][r];
-            *reinterpret_cast<float2 *>(&S.stage[1][sl][cy + r][cx]) = out[r];
-        }
-        if (sl == 3) s2_encode_slab<TY, ENC>(S, a, x0, y0, z - 3);
-    }
+    float *dst = a.pprev + (int64_t)z * a.pstride + g0;
+    if (okr0) __stcs(reinterpret_cast<float2 *>(dst), out[0]);
+    if (okr1) __stcs(reinterpret_cast<float2 *>(dst + a.pitch), out[1]);
     return true;
 }
 
-// encode the staged 4-plane slab (planes zslab..zslab+3) of both arrays: 2 arrays x TY/4 block rows x
-// 2 groups of 8 x-adjacent blocks; every warp first loads the rows of its tasks, then (the staging is
-// reused as code scratch) encodes them with the standalone encoder's core
-template <int TY, int ENC>
-__device__ __noinline__ void s2_encode_slab(S2Smem<TY, ENC> &S, const StepArgs &a, int x0, int y0, int zslab) {
-    if constexpr (ENC) {
-        constexpr int NW = S2T<TY>::THREADS / 32, NT = 2 * (TY / 4) * 2, TPW = NT / NW;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int ib = lane & 7, r0 = lane >> 3;
-        __syncthreads();  // the whole slab is staged
-        float4 v[TPW][4];
-        bool live[TPW];
-        int arr[TPW], byl[TPW], bxl0[TPW];
-#pragma unroll
-        for (int j = 0; j < TPW; ++j) {
-            const int tk = warp + j * NW;
-            arr[j] = tk / (2 * (TY / 4));
-            byl[j] = (tk >> 1) % (TY / 4);
-            bxl0[j] = 8 * (tk & 1);
-            const int bxl = bxl0[j] + ib;
-            live[j] = x0 + 4 * bxl < a.nx && y0 + 4 * byl[j] < a.ny;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int r = r0 + 4 * u;  // yi = r & 3, zi = r >> 2
-                v[j][u] = *reinterpret_cast<const float4 *>(&S.stage[arr[j]][r >> 2][4 * byl[j] + (r & 3)][4 * bxl]);
-            }
-        }
-        __syncthreads();  // staging now free: reuse it as per-warp code scratch
-        uint32_t(*cw)[CODE_LD] = reinterpret_cast<uint32_t(*)[CODE_LD]>(&S.stage[0][0][0][0]) + warp * 8;
-        const int recw = 2 * (a.q + 1);
-        bool bad = false;
-#pragma unroll
-        for (int j = 0; j < TPW; ++j) {
-            const uint32_t mask = __ballot_sync(0xffffffffu, live[j] && r0 == 0) & 0xFFu;
-            const int bz = (zslab - a.z_lo) >> 2;
-            const int by = 1 + (y0 >> 2) + byl[j], bx = 1 + (x0 >> 2) + bxl0[j];
-            uint32_t *rec0 = a.out[arr[j]] + ((int64_t)(bz * a.nby + by) * a.nbx + bx) * recw;
-            if constexpr (ENC == ENC_Q15)
-                bad |= bq_encode_core<false, 15>(v[j], live[j], mask, rec0, 15, cw, lane);
-            else if constexpr (ENC == ENC_TWO)
-                bad |= bq_encode_core<true, 0>(v[j], live[j], mask, rec0, a.q, cw, lane);
-            else
-                bad |= bq_encode_core<false, 0>(v[j], live[j], mask, rec0, a.q, cw, lane);
-        }
-        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1);
-    }
-}
-
-template <int TY, int ENC>
+template <int TY>
 __global__ void __launch_bounds__(S2T<TY>::THREADS, S2T<TY>::CTAS)
 stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mPP,
                         const __grid_constant__ CUtensorMap mV, const StepArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    S2Smem<TY, ENC> &S = *reinterpret_cast<S2Smem<TY, ENC> *>(smem_raw);
+    S2Smem<TY> &S = *reinterpret_cast<S2Smem<TY> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int x0 = blockIdx.x * S2_TX, y0 = blockIdx.y * TY;
     const int zs = a.z_lo + blockIdx.z * a.zchunk;
@@ -742,7 +651,7 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
         // first D stages (plane z+4 of p_curr, plane z of p_prev and v)
         unsigned long long *pro = &S.bar[S2_NB];
         mbar_expect_tx(pro, 4 * S2T<TY>::PBYTES);
-        constexpr int NS = s2_ring<ENC>();
+        constexpr int NS = S2_NS;
         for (int i = 0; i < 4; ++i) tma_load_3d(&S.p[(4 + i) % NS][0][0], &mP, XOFF + x0, y0, zs + i, pro);
         for (int j = 0; j < S2_D; ++j) {
             const int z = zs + j;
@@ -769,15 +678,15 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
     mbar_wait(&S.bar[S2_NB], 0);
     uint32_t ph = 0;
     for (int zb = zs; zb < ze; zb += 9) {
-        if (!s2_plane<0, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<1, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<2, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<3, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<4, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<5, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<6, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<7, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<8, TY, ENC>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<0, TY>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<1, TY>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<2, TY>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<3, TY>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<4, TY>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<5, TY>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<6, TY>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<7, TY>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<8, TY>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
     }
 }
 
@@ -1241,7 +1150,7 @@ cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, 
         }
         A.slabs = (int)(planes / 4);
         const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(A.slabs * n_arr));
-#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 0)
+#define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err)
         switch (q) {
         case 7: ENC(false, 7); break;
         case 11: ENC(false, 11); break;
@@ -1350,14 +1259,14 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t pitch, int64_t a
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TY, int ENC>
+template <int TY>
 static cudaError_t launch_stencil(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay,
                                   int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, StepArgs a,
                                   cudaStream_t st) {
     if (z_hi <= z_lo) return cudaSuccess;
-    const size_t smem = sizeof(S2Smem<TY, ENC>);
+    const size_t smem = sizeof(S2Smem<TY>);
     // per device (the attribute is per function and device); idempotent, so racing threads are harmless
-    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel<TY, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mP, mPP, mV;
@@ -1375,13 +1284,12 @@ static cudaError_t launch_stencil(const float *vel, float *pprev, const float *p
     a.dt = dt;
     const int gx = (a.nx + S2_TX - 1) / S2_TX, gy = (a.ny + TY - 1) / TY;
     a.gx = gx;
-    // split z so the grid is close to a whole number of waves; the encoding variant splits on 4-plane slabs
+    // split z so the grid is close to a whole number of waves
     const int Z = (int)(z_hi - z_lo), tiles = gx * gy, res = 148 * S2T<TY>::CTAS;
-    const int unit = ENC ? 4 : 1;
     int best = 1;
     double best_eff = 0;
     for (int nzc = 1; nzc <= 16; ++nzc) {
-        const int chunk = ((Z + nzc - 1) / nzc + unit - 1) / unit * unit;
+        const int chunk = (Z + nzc - 1) / nzc;
         if (nzc > 1 && chunk < 24) break;
         const int items = tiles * ((Z + chunk - 1) / chunk);
         const double waves = (double)items / res;
@@ -1391,10 +1299,10 @@ static cudaError_t launch_stencil(const float *vel, float *pprev, const float *p
             best = nzc;
         }
     }
-    a.zchunk = ((Z + best - 1) / best + unit - 1) / unit * unit;
+    a.zchunk = (Z + best - 1) / best;
     const int nzc = (Z + a.zchunk - 1) / a.zchunk;
     dim3 grid(gx, gy, nzc);
-    stencil_step_tma_kernel<TY, ENC><<<grid, S2T<TY>::THREADS, smem, st>>>(mP, mPP, mV, a);
+    stencil_step_tma_kernel<TY><<<grid, S2T<TY>::THREADS, smem, st>>>(mP, mPP, mV, a);
     return cudaGetLastError();
 }
 
@@ -1430,346 +1338,6 @@ __global__ void __launch_bounds__(256) star7_step_kernel(const float *__restrict
     }
 }
 
-// ---------------------------------------------------------------------------
-// Two leapfrog steps fused (NEXT-2, SURVEY §8(f) "2-step register blocking"; P:L233 / P:L254 "optimizing
-// GPU computation"), out of place:
-//     C = p(t+1) = step(A = p(t-1), B = p(t))  on planes [z1lo, z1hi)
-//     D = p(t+2) = step(B, C)                  on planes [z2lo, z2hi)
-// per cell-update pair 12 B read (A, B, v) + 8 B written (C, D) = 10 B per update instead of 16.
-// A CTA owns a 64 x 16 tile of D and marches z.  Level t+1 is computed on the tile plus its R halo
-// (72 x 24, "ext"), plane z1 = z + 4 ahead of the level-t+2 plane z: its x/y neighbours come from a TMA
-// ring of B boxes with a 2R halo (80 x 32), its z neighbours from per-thread register queues (own 2 x 2
-// cells and up to two halo pairs per thread); the finished level-t+1 plane goes to a shared ring Q (the
-// x/y neighbours of step 2) and, for the thread's own cells, into a second register queue (step 2's z
-// neighbours).  Ext cells outside the domain or planes outside [z1lo, z1hi) take B's value (Dirichlet:
-// every level holds the initial boundary values).  Every operation is the single-step kernel's
-// (difference form, paired fp32, same order), so the results are bitwise those of two oocs_step calls.
-// C and D are written on interior cells only: their halo (x/y ring, boundary planes) is the caller's.
-// ---------------------------------------------------------------------------
-namespace st2 {
-constexpr int TX = 64, TY = 16, THREADS = 256;
-constexpr int EW = TX + 2 * R, EH = TY + 2 * R;          // ext tile (level t+1), 72 x 24
-constexpr int BW = TX + 4 * R, BH = TY + 4 * R;          // B box, 80 x 32
-constexpr int NS = 9, NB = 3, D = 2;                     // ring slots, A/V stages, prefetch distance
-constexpr int HALO_PAIRS = (EW / 2) * EH - (TX / 2) * TY;  // 352 float2 pairs of ext outside the tile
-constexpr uint32_t BBYTES = BW * BH * 4, EBYTES = EW * EH * 4;
-struct Smem {
-    float b[NS][BH][BW];
-    float q[NS][EH][EW];
-    float a[NB][EH][EW];
-    float v[NB][EH][EW];
-    unsigned long long bar[NB + 1];
-};
-struct Args {
-    const float *A, *B, *V;
-    float *C, *D;
-    int nx, ny, ax, ay, planes;
-    int z1lo, z1hi, z2lo, z2hi, zchunk;
-    int64_t pitch, pstride;
-    float dt;
-};
-// ext coordinates (ex, ey) of halo pair j (row-major over the 4 full rows above and below the tile, then
-// the 16 rows' left / right 4-column strips)
-__device__ __forceinline__ void halo_pair(int j, int &ex, int &ey) {
-    if (j < 8 * (EW / 2)) {
-        const int row = j / (EW / 2);
-        ey = row < R ? row : row + TY;
-        ex = 2 * (j % (EW / 2));
-    } else {
-        const int k = j - 8 * (EW / 2);
-        ey = R + (k >> 2);
-        const int side = k & 3;
-        ex = side < 2 ? 2 * side : TX + R + 2 * (side - 2);
-    }
-}
-}  // namespace st2
-
-// the difference-form Laplacian of one pair row (x neighbours from a box row, y neighbours given, z from
-// a queue) -- the single-step kernel's operation order exactly
-#define ST2_LAP(lap, P, row, col, yl, yh, QZ, r, OFF)                                                        \
-    do {                                                                                                     \
-        const float2 xa = *reinterpret_cast<const float2 *>(&P[row][col]);                                 \
-        const float2 xb = *reinterpret_cast<const float2 *>(&P[row][col + 2]);                             \
-        const float2 xc = *reinterpret_cast<const float2 *>(&P[row][col + 6]);                             \
-        const float2 xd = *reinterpret_cast<const float2 *>(&P[row][col + 8]);                             \
-        const float2 f0 = QZ[((OFF) + 4) % 9] r;                                                             \
-        const float2 f2 = __fadd2_rn(f0, f0);                                                                \
-        const float2 nf2 = make_float2(-f2.x, -f2.y);                                                        \
-        auto d = [&](float2 lo, float2 hi) { return __fadd2_rn(__fadd2_rn(lo, hi), nf2); };                  \
-        lap = __fmul2_rn(k1, d(make_float2(xb.y, f0.x), make_float2(f0.y, xc.x)));                           \
-        lap = __ffma2_rn(k2, d(xb, xc), lap);                                                                \
-        lap = __ffma2_rn(k3, d(make_float2(xa.y, xb.x), make_float2(xc.y, xd.x)), lap);                      \
-        lap = __ffma2_rn(k4, d(xa, xd), lap);                                                                \
-        lap = __ffma2_rn(k1, d(yl[3], yh[5]), lap);                                                          \
-        lap = __ffma2_rn(k2, d(yl[2], yh[6]), lap);                                                          \
-        lap = __ffma2_rn(k3, d(yl[1], yh[7]), lap);                                                          \
-        lap = __ffma2_rn(k4, d(yl[0], yh[8]), lap);                                                          \
-        lap = __ffma2_rn(k1, d(QZ[((OFF) + 3) % 9] r, QZ[((OFF) + 5) % 9] r), lap);                          \
-        lap = __ffma2_rn(k2, d(QZ[((OFF) + 2) % 9] r, QZ[((OFF) + 6) % 9] r), lap);                          \
-        lap = __ffma2_rn(k3, d(QZ[((OFF) + 1) % 9] r, QZ[((OFF) + 7) % 9] r), lap);                          \
-        lap = __ffma2_rn(k4, d(QZ[((OFF) + 0) % 9] r, QZ[((OFF) + 8) % 9] r), lap);                          \
-    } while (0)
-
-__device__ __forceinline__ float2 st2_update(float2 lap, float2 f0, float2 pv, float2 vv, float dt) {
-    const float2 f2 = __fadd2_rn(f0, f0);
-    const float2 vd = __fmul2_rn(vv, make_float2(dt, dt));
-    return __ffma2_rn(__fmul2_rn(vd, vd), lap, __fadd2_rn(f2, make_float2(-pv.x, -pv.y)));
-}
-
-template <int OFF>
-__device__ __forceinline__ bool st2_plane(st2::Smem &S, const CUtensorMap *mB, const CUtensorMap *mA,
-                                          const CUtensorMap *mV, const st2::Args &a, int z1, int zs1, int ze1,
-                                          int zs2, int ze2, int x0, int y0, float2 (&q)[9][2], float2 (&g)[9][2],
-                                          float2 (&h)[2][9], uint32_t &ph, int hx0, int hy0, int hx1, int hy1,
-                                          bool hv0, bool hv1) {
-    using namespace st2;
-    if (z1 >= ze1) return false;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __syncthreads();  // plane z1-1 is done everywhere: its ring slots may be refilled
-    if (tid == 0 && z1 + D < ze1) {
-        constexpr int ps = (OFF + 4 + D + R) % NS, st = (OFF + D) % NB;
-        unsigned long long *bar = &S.bar[st];
-        mbar_expect_tx(bar, BBYTES + 2 * EBYTES);
-        tma_load_3d(&S.b[ps][0][0], mB, XOFF - R + x0, y0 - R, z1 + D + R, bar);
-        tma_load_3d(&S.a[st][0][0], mA, XOFF + x0, y0, z1 + D, bar);
-        tma_load_3d(&S.v[st][0][0], mV, XOFF + x0, y0, z1 + D, bar);
-    }
-    constexpr int st = OFF % NB, sz = (OFF + 4) % NS, sz4 = (OFF + 8) % NS;
-    mbar_wait(&S.bar[st], (ph >> st) & 1u);
-    ph ^= 1u << st;
-    const float2 k1 = make_float2(C1, C1), k2 = make_float2(C2, C2), k3 = make_float2(C3, C3),
-                 k4 = make_float2(C4, C4);
-    const bool in1 = z1 >= a.z1lo && z1 < a.z1hi;
-    const float(*P)[BW] = S.b[sz];
-    const int cx = 2 * lane, cy = 2 * warp;
-    // ---- step 1, own 2 x 2 cells (box (cx+8, cy+8)): feed the queue with plane z1+4
-    q[(OFF + 8) % 9][0] = *reinterpret_cast<const float2 *>(&S.b[sz4][2 * R + cy][2 * R + cx]);
-    q[(OFF + 8) % 9][1] = *reinterpret_cast<const float2 *>(&S.b[sz4][2 * R + cy + 1][2 * R + cx]);
-    {
-        float2 yr[10];
-#pragma unroll
-        for (int m = 0; m < 10; ++m)
-            if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&P[R + cy + m][2 * R + cx]);
-        yr[4] = q[(OFF + 4) % 9][0];
-        yr[5] = q[(OFF + 4) % 9][1];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            float2 lap;
-            ST2_LAP(lap, P, 2 * R + cy + r, R + cx, (yr + r), (yr + r), q, [r], OFF);
-            const float2 pv = *reinterpret_cast<const float2 *>(&S.a[st][R + cy + r][R + cx]);
-            const float2 vv = *reinterpret_cast<const float2 *>(&S.v[st][R + cy + r][R + cx]);
-            const float2 f0 = q[(OFF + 4) % 9][r];
-            const int x = x0 + cx, y = y0 + cy + r;
-            float2 o = st2_update(lap, f0, pv, vv, a.dt);
-            // out of the domain (the R-cell halo and beyond) or outside [z1lo, z1hi): B's value
-            if (!in1 || y >= a.ny) o = f0;
-            else if (x + 1 >= a.nx) o = make_float2(x < a.nx ? o.x : f0.x, f0.y);
-            g[(OFF + 8) % 9][r] = o;
-            *reinterpret_cast<float2 *>(&S.q[OFF % NS][R + cy + r][R + cx]) = o;
-            if (in1 && z1 >= a.z1lo && y < a.ny && x < a.nx) {
-                // C: own cells of the planes this CTA is responsible for
-                const bool mine = (z1 >= zs2 || zs2 == a.z2lo) && (z1 < ze2 || ze2 == a.z2hi);
-                if (mine) {
-                    float *dst = a.C + (int64_t)z1 * a.pstride + (int64_t)(y + R) * a.pitch + x + R + XOFF;
-                    if (x + 1 < a.nx) __stcs(reinterpret_cast<float2 *>(dst), o);
-                    else *dst = o.x;
-                }
-            }
-        }
-    }
-    // ---- step 1, halo pairs: one row each
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const bool hv = j ? hv1 : hv0;
-        const int ex = j ? hx1 : hx0, ey = j ? hy1 : hy0;
-        if (!hv) continue;
-        h[j][(OFF + 8) % 9] = *reinterpret_cast<const float2 *>(&S.b[sz4][R + ey][R + ex]);
-        float2 yv[9];
-#pragma unroll
-        for (int m = 0; m < 9; ++m)
-            if (m != 4) yv[m] = *reinterpret_cast<const float2 *>(&P[ey + m][R + ex]);
-        const float2 f0 = h[j][(OFF + 4) % 9];
-        float2 lap;
-        {
-            const float2 xa = *reinterpret_cast<const float2 *>(&P[R + ey][ex]);
-            const float2 xb = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 2]);
-            const float2 xc = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 6]);
-            const float2 xd = *reinterpret_cast<const float2 *>(&P[R + ey][ex + 8]);
-            const float2 f2 = __fadd2_rn(f0, f0);
-            const float2 nf2 = make_float2(-f2.x, -f2.y);
-            auto d = [&](float2 lo, float2 hi) { return __fadd2_rn(__fadd2_rn(lo, hi), nf2); };
-            lap = __fmul2_rn(k1, d(make_float2(xb.y, f0.x), make_float2(f0.y, xc.x)));
-            lap = __ffma2_rn(k2, d(xb, xc), lap);
-            lap = __ffma2_rn(k3, d(make_float2(xa.y, xb.x), make_float2(xc.y, xd.x)), lap);
-            lap = __ffma2_rn(k4, d(xa, xd), lap);
-            lap = __ffma2_rn(k1, d(yv[3], yv[5]), lap);
-            lap = __ffma2_rn(k2, d(yv[2], yv[6]), lap);
-            lap = __ffma2_rn(k3, d(yv[1], yv[7]), lap);
-            lap = __ffma2_rn(k4, d(yv[0], yv[8]), lap);
-            lap = __ffma2_rn(k1, d(h[j][(OFF + 3) % 9], h[j][(OFF + 5) % 9]), lap);
-            lap = __ffma2_rn(k2, d(h[j][(OFF + 2) % 9], h[j][(OFF + 6) % 9]), lap);
-            lap = __ffma2_rn(k3, d(h[j][(OFF + 1) % 9], h[j][(OFF + 7) % 9]), lap);
-            lap = __ffma2_rn(k4, d(h[j][(OFF + 0) % 9], h[j][(OFF + 8) % 9]), lap);
-        }
-        const float2 pv = *reinterpret_cast<const float2 *>(&S.a[st][ey][ex]);
-        const float2 vv = *reinterpret_cast<const float2 *>(&S.v[st][ey][ex]);
-        float2 o = st2_update(lap, f0, pv, vv, a.dt);
-        const int x = x0 + ex - R, y = y0 + ey - R;
-        const bool yin = y >= 0 && y < a.ny;
-        const bool x0in = x >= 0 && x < a.nx, x1in = x + 1 >= 0 && x + 1 < a.nx;
-        if (!in1 || !yin) o = f0;
-        else o = make_float2(x0in ? o.x : f0.x, x1in ? o.y : f0.y);
-        *reinterpret_cast<float2 *>(&S.q[OFF % NS][ey][ex]) = o;
-    }
-    // ---- step 2 at plane z = z1 - 4: x/y neighbours from Q plane z (written 4 iterations ago), z from g
-    const int z = z1 - R;
-    if (z >= zs2 && z < ze2) {
-        const float(*Q)[EW] = S.q[(OFF + 5) % NS];
-        float2 yr[10];
-#pragma unroll
-        for (int m = 0; m < 10; ++m)
-            if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&Q[cy + m][R + cx]);
-        yr[4] = g[(OFF + 4) % 9][0];
-        yr[5] = g[(OFF + 4) % 9][1];
-        const int x = x0 + cx;
-        const int64_t g0 = (int64_t)(y0 + cy + R) * a.pitch + x + R + XOFF;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int y = y0 + cy + r;
-            if (y >= a.ny || x >= a.nx) continue;
-            float2 lap;
-            ST2_LAP(lap, Q, R + cy + r, cx, (yr + r), (yr + r), g, [r], OFF);
-            const float *vp = a.V + (int64_t)z * a.pstride + g0 + r * a.pitch;
-            const float2 vv = x + 1 < a.nx ? __ldg(reinterpret_cast<const float2 *>(vp)) : make_float2(__ldg(vp), 0.f);
-            const float2 o = st2_update(lap, g[(OFF + 4) % 9][r], q[OFF % 9][r], vv, a.dt);
-            float *dst = a.D + (int64_t)z * a.pstride + g0 + r * a.pitch;
-            if (x + 1 < a.nx) __stcs(reinterpret_cast<float2 *>(dst), o);
-            else *dst = o.x;
-        }
-    }
-    return true;
-}
-
-__global__ void __launch_bounds__(st2::THREADS, 1)
-stencil_step2_kernel(const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mA,
-                     const __grid_constant__ CUtensorMap mV, const st2::Args a) {
-    using namespace st2;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zs2 = a.z2lo + blockIdx.z * a.zchunk, ze2 = min(a.z2hi, zs2 + a.zchunk);
-    if (zs2 >= ze2) return;
-    const int zs1 = zs2 - R, ze1 = ze2 + R;  // level t+1 planes this CTA computes (B's copy outside [z1lo, z1hi))
-    if (tid == 0) {
-        for (int i = 0; i <= NB; ++i) mbar_init(&S.bar[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-        unsigned long long *pro = &S.bar[NB];
-        mbar_expect_tx(pro, 4 * BBYTES);
-        for (int i = 0; i < 4; ++i) tma_load_3d(&S.b[(4 + i) % NS][0][0], &mB, XOFF - R + x0, y0 - R, zs1 + i, pro);
-        for (int j = 0; j < D; ++j) {
-            unsigned long long *bar = &S.bar[j % NB];
-            mbar_expect_tx(bar, BBYTES + 2 * EBYTES);
-            tma_load_3d(&S.b[(j + 4 + R) % NS][0][0], &mB, XOFF - R + x0, y0 - R, zs1 + j + R, bar);
-            tma_load_3d(&S.a[j % NB][0][0], &mA, XOFF + x0, y0, zs1 + j, bar);
-            tma_load_3d(&S.v[j % NB][0][0], &mV, XOFF + x0, y0, zs1 + j, bar);
-        }
-    }
-    // halo pairs of this thread, and the register queues of B (planes zs1-4 .. zs1+3) from global memory;
-    // cells outside the allocated grid or planes outside the buffer read as 0 (never used for a result)
-    int hx0 = 0, hy0 = 0, hx1 = 0, hy1 = 0;
-    const bool hv0 = tid < HALO_PAIRS, hv1 = tid + THREADS < HALO_PAIRS;
-    if (hv0) halo_pair(tid, hx0, hy0);
-    if (hv1) halo_pair(tid + THREADS, hx1, hy1);
-    auto ldq = [&](int ex, int ey, int z) -> float2 {
-        // ext (ex, ey) -> allocated column x0 + ex (interior x0 + ex - R), row y0 + ey
-        const int ac = x0 + ex, ar = y0 + ey;
-        if (z < 0 || z >= a.planes || ar < 0 || ar >= a.ay || ac < 0 || ac + 1 >= a.ax + 1) return make_float2(0.f, 0.f);
-        const float *p = a.B + (int64_t)z * a.pstride + (int64_t)ar * a.pitch + XOFF + ac;
-        return ac + 1 < a.ax ? __ldg(reinterpret_cast<const float2 *>(p)) : make_float2(__ldg(p), 0.f);
-    };
-    float2 q[9][2], g[9][2], h[2][9];
-    const int cx = 2 * lane, cy = 2 * warp;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        const int z = zs1 - R + m;
-        q[m][0] = ldq(R + cx, R + cy, z);
-        q[m][1] = ldq(R + cx, R + cy + 1, z);
-        h[0][m] = hv0 ? ldq(hx0, hy0, z) : make_float2(0.f, 0.f);
-        h[1][m] = hv1 ? ldq(hx1, hy1, z) : make_float2(0.f, 0.f);
-        g[m][0] = g[m][1] = make_float2(0.f, 0.f);
-    }
-    q[8][0] = q[8][1] = h[0][8] = h[1][8] = g[8][0] = g[8][1] = make_float2(0.f, 0.f);
-    mbar_wait(&S.bar[NB], 0);
-    uint32_t ph = 0;
-    for (int zb = zs1; zb < ze1; zb += 9) {
-#define ST2P(O)                                                                                                 \
-    if (!st2_plane<O>(S, &mB, &mA, &mV, a, zb + O, zs1, ze1, zs2, ze2, x0, y0, q, g, h, ph, hx0, hy0, hx1, hy1, \
-                      hv0, hv1))                                                                               \
-        break;
-        ST2P(0) ST2P(1) ST2P(2) ST2P(3) ST2P(4) ST2P(5) ST2P(6) ST2P(7) ST2P(8)
-#undef ST2P
-    }
-}
-#undef ST2_LAP
-
-cudaError_t launch_step2(const float *vel, const float *A, const float *B, float *C, float *Dd, int64_t ax, int64_t ay,
-                         int64_t pitch, int64_t planes, int64_t z1lo, int64_t z1hi, int64_t z2lo, int64_t z2hi,
-                         float dt, cudaStream_t st) {
-    using namespace st2;
-    if (z2hi <= z2lo) return cudaSuccess;
-    // step 1 must cover what step 2 reads: [z2lo - R, z2hi + R) within [z1lo, z1hi) except Dirichlet planes
-    if (z1lo > z2lo || z1hi < z2hi || z2lo - z1lo > R || z1hi - z2hi > R || z1lo < R || z1hi > planes - R)
-        return cudaErrorInvalidValue;
-    const size_t smem = sizeof(Smem);
-    cudaError_t e = cudaFuncSetAttribute(stencil_step2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    CUtensorMap mB, mA, mV;
-    if (!make_map(&mB, B, pitch, ay, planes, BW, BH) || !make_map(&mA, A, pitch, ay, planes, EW, EH) ||
-        !make_map(&mV, vel, pitch, ay, planes, EW, EH))
-        return cudaErrorInvalidValue;
-    Args a{};
-    a.A = A;
-    a.B = B;
-    a.V = vel;
-    a.C = C;
-    a.D = Dd;
-    a.nx = (int)(ax - 2 * R);
-    a.ny = (int)(ay - 2 * R);
-    a.ax = (int)ax;
-    a.ay = (int)ay;
-    a.planes = (int)planes;
-    a.z1lo = (int)z1lo;
-    a.z1hi = (int)z1hi;
-    a.z2lo = (int)z2lo;
-    a.z2hi = (int)z2hi;
-    a.pitch = pitch;
-    a.pstride = ay * pitch;
-    a.dt = dt;
-    const int gx = (a.nx + TX - 1) / TX, gy = (a.ny + TY - 1) / TY;
-    const int Z = (int)(z2hi - z2lo), tiles = gx * gy;
-    // z split: whole waves of 148 CTAs (1 per SM), each extra split costs 2R redundant level-(t+1) planes
-    int best = 1;
-    double best_eff = 0;
-    for (int nzc = 1; nzc <= 16; ++nzc) {
-        const int chunk = (Z + nzc - 1) / nzc;
-        if (nzc > 1 && chunk < 24) break;
-        const double waves = (double)tiles * ((Z + chunk - 1) / chunk) / 148.0;
-        const double eff = waves / std::ceil(waves) * (double)chunk / (chunk + 2.0 * R + 4.0);
-        if (eff > best_eff + 1e-3) {
-            best_eff = eff;
-            best = nzc;
-        }
-    }
-    a.zchunk = (Z + best - 1) / best;
-    const dim3 grid(gx, gy, (Z + a.zchunk - 1) / a.zchunk);
-    stencil_step2_kernel<<<grid, THREADS, smem, st>>>(mB, mA, mV, a);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int stencil, cudaStream_t st) {
     if (stencil == OOCS_STENCIL_STAR7) {
@@ -1784,7 +1352,7 @@ cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int6
         return cudaGetLastError();
     }
     StepArgs a{};
-    return launch_stencil<16, ENC_NONE>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+    return launch_stencil<16>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
 }
 
 // max |x| over rows of n floats (CFL check of a loaded velocity); float bits of non-negative values order
@@ -1809,46 +1377,5 @@ cudaError_t launch_absmax(const float *src, int64_t rows, int64_t n, int64_t pit
     return cudaGetLastError();
 }
 
-cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,
-                               int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
-                               void *out_prev, void *out_curr, int *err, cudaStream_t st) {
-    if ((z_lo | z_hi) & 3) return cudaErrorInvalidValue;  // whole 4-plane slabs
-    StepArgs a{};
-    a.out[0] = static_cast<uint32_t *>(out_prev);
-    a.out[1] = static_cast<uint32_t *>(out_curr);
-    a.nbx = (int)(ax / 4);
-    a.nby = (int)(ay / 4);
-    a.q = q;
-    a.err = err;
-    float *pp = const_cast<float *>(pprev);
-    cudaError_t e = q == 15  ? launch_stencil<16, ENC_Q15>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st)
-                    : q > 16 ? launch_stencil<16, ENC_TWO>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st)
-                             : launch_stencil<16, ENC_ONE>(vel, pp, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
-    if (e != cudaSuccess) return e;
-    // the x/y halo blocks of the owned slabs (constant Dirichlet values, same in both arrays) are not
-    // produced by the fused kernel: encode them with the standalone encoder's edge modes
-    const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
-    const int nl = (int)nlines_of(ax);
-    const int64_t pstride = ay * pitch;
-    const int slabs = (int)((z_hi - z_lo) / 4);
-    const float *src = pcurr + z_lo * pstride;
-    // both arrays in each launch (same source: the halo values are level-independent)
-    CodecArrays A{};
-    A.src[0] = A.src[1] = src;
-    A.dst[0] = out_prev;
-    A.dst[1] = out_curr;
-    A.slabs = slabs;
-    const dim3 gx2(2, (unsigned)((nby + 7) / 8), (unsigned)(2 * slabs)), gy2((unsigned)nl, 1, (unsigned)(2 * slabs));
-#define EDGE(TWO, QT)                                                                                        \
-    do {                                                                                                     \
-        bq_encode_kernel<TWO, QT><<<gx2, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 1); \
-        bq_encode_kernel<TWO, QT><<<gy2, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err, 2); \
-    } while (0)
-    if (q == 15) EDGE(false, 15);
-    else if (q > 16) EDGE(true, 0);
-    else EDGE(false, 0);
-#undef EDGE
-    return cudaGetLastError();
-}
 
 }  // namespace oocs

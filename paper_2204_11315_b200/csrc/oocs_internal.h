@@ -50,17 +50,9 @@ cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, 
                           int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int stencil, cudaStream_t st);
-// two fused leapfrog steps, out of place (oocs.h oocs_step2)
-cudaError_t launch_step2(const float *vel, const float *A, const float *B, float *C, float *D, int64_t ax, int64_t ay,
-                         int64_t pitch, int64_t planes, int64_t z1lo, int64_t z1hi, int64_t z2lo, int64_t z2hi,
-                         float dt, cudaStream_t st);
 // max |x| over `rows` rows of `n` floats (row stride `pitch` floats) folded into *out (float bits as u32,
 // atomicMax; NaN compares above +Inf); *out must be initialised by the caller
 cudaError_t launch_absmax(const float *src, int64_t rows, int64_t n, int64_t pitch, uint32_t *out, cudaStream_t st);
-// last step fused with the BlockQuant encode of the owned slabs [z_lo, z_hi) (device store)
-cudaError_t launch_step_encode(const float *vel, const float *pprev, const float *pcurr, int64_t ax, int64_t ay,
-                               int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
-                               void *out_prev, void *out_curr, int *err, cudaStream_t st);
 
 // multi-GPU halo send: two equal-length byte ranges (8-byte multiples), dst possibly peer memory
 cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, void *dst1, uint64_t bytes,

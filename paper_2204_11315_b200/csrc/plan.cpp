@@ -51,6 +51,9 @@ static bool validate(const oocs_config *c, std::string *err) {
     if (c->world > 1 && c->mode == OOCS_MODE_BASELINE)
         return bad(err, "the uncompressed BASELINE (fig:3ver(a)) is a single-GPU comparison: world must be 1");
     if (c->device < 0) return bad(err, "bad device ordinal");
+    if (c->flags & ~(uint32_t)(OOCS_FLAG_PROFILE | OOCS_FLAG_RESIDENT_VELOCITY | OOCS_FLAG_TIMELINE |
+                               OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS | OOCS_FLAG_DECODED_VELOCITY))
+        return bad(err, "unknown or retired flag (4 = ABI 1's fused last step + encode, removed)");
     if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
         return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
     if ((c->flags & OOCS_FLAG_DECODED_VELOCITY) && c->store != OOCS_STORE_DEVICE)

@@ -303,30 +303,6 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
     return OOCS_OK;
 }
 
-// device store + BlockQuant, opted in: the last step of a chunk is fused with the encode
-static bool fuse_last_step(const Plan *p) {
-    const Geometry &g = p->geo;
-    return !g.host_store && g.codec == OOCS_CODEC_BLOCKQUANT && (g.cfg.flags & OOCS_FLAG_FUSE_ENCODE) &&
-           g.cfg.stencil == OOCS_STENCIL_ACOUSTIC25;
-}
-
-static oocs_status k_step_encode(Plan *p, const float *v, const float *pp, const float *pc, int64_t zlo, int64_t zhi,
-                                 void *out_prev, void *out_curr, cudaStream_t st, oocs_stats *stats) {
-    KernelTiming *t = timing_slot(p, 1);
-    if (t) CU(cudaEventRecord(t->a, st));
-    CU(launch_step_encode(v, pp, pc, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi, p->geo.cfg.dt,
-                          p->geo.q, out_prev, out_curr, p->d_err, st));
-    if (t) CU(cudaEventRecord(t->b, st));
-    if (stats) {
-        stats->kernel_launches[1]++;
-        const uint64_t cells = (uint64_t)(zhi - zlo) * p->geo.nx * p->geo.ny;
-        stats->cell_updates_computed += cells;
-        // read p_curr, p_prev, v (12 B); write two compressed values (2 r/8 B)
-        stats->alg_bytes[1] += cells * 12 + (uint64_t)(zhi - zlo) * 2 * pb(p);
-    }
-    return OOCS_OK;
-}
-
 // ---------------------------------------------------------------------------
 // plan create / destroy
 // ---------------------------------------------------------------------------
@@ -729,23 +705,12 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
         const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
         const int up = upd_array(sidx), other = 3 - up;
-        if (fuse_last_step(p) && sidx == g.k) {
-            // the last step and the encode of the owned slabs in one kernel: level k is never
-            // written back, (level k-1, level k) go straight to S_{t+1}'s records
-            void *out_prev = p->dstore[p->cur ^ 1][1] + hoff(p, b.own_lo);
-            void *out_curr = p->dstore[p->cur ^ 1][2] + hoff(p, b.own_lo);
-            oocs_status r = k_step_encode(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
-                                          hi - b.ext_lo, out_prev, out_curr, st, stats);
-            if (r) return r;
-            break;
-        }
         oocs_status r = k_step(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo,
                                st, stats);
         if (r) return r;
         break;
     }
     case OOCS_OP_ENCODE: {
-        if (fuse_last_step(p)) break;  // done by the fused last step
         // after k steps: level t0+k in array upd(k), level t0+k-1 in the other
         const int curr = upd_array(g.k), prev = 3 - curr;
         const int64_t W = b.own_hi - b.own_lo, off = b.own_lo - b.ext_lo;
@@ -1621,19 +1586,6 @@ oocs_status oocs_step(const float *vel, float *p_prev, const float *p_curr, int6
         return OOCS_ERR_CONFIG;
     }
     CU(launch_step(vel, p_prev, p_curr, ax, ay, pitch, planes, z_lo, z_hi, dt, stencil, (cudaStream_t)stream));
-    return OOCS_OK;
-}
-
-oocs_status oocs_step2(const float *vel, const float *A, const float *B, float *C, float *D, int64_t ax, int64_t ay,
-                       int64_t planes, int64_t pitch, float dt, int64_t z1_lo, int64_t z1_hi, int64_t z2_lo,
-                       int64_t z2_hi, void *stream) {
-    if (ax % 4 || ay % 4 || pitch < ax + XOFF || pitch % 32 || z1_lo < R || z1_hi > planes - R || z1_lo > z2_lo ||
-        z2_lo - z1_lo > R || z2_hi > z1_hi || z1_hi - z2_hi > R || z2_lo > z2_hi || !A || !B || !C || !D || !vel ||
-        C == A || C == B || D == A || D == B || C == D) {
-        set_error("oocs_step2: bad geometry, plane ranges or aliasing");
-        return OOCS_ERR_CONFIG;
-    }
-    CU(launch_step2(vel, A, B, C, D, ax, ay, pitch, planes, z1_lo, z1_hi, z2_lo, z2_hi, dt, (cudaStream_t)stream));
     return OOCS_OK;
 }
 

@@ -404,35 +404,12 @@ def test_degenerate_cases():
     a1.close()
 
 
-@pytest.mark.parametrize("rate", [8, 12, 16, 24])
-@pytest.mark.parametrize("nx,ny,nz,n,k", [(40, 32, 64, 4, 2), (72, 44, 48, 3, 1), (132, 100, 96, 2, 3)])
-def test_fused_last_step_encode_bitwise(rate, nx, ny, nz, n, k):
-    """Device store: the last step fused with the encode (incl. the halo-block edge encodes) writes the
-    same S_{t+1} bytes as the separate step + encode kernels."""
-    vel, p0 = synth.fields(nx, ny, nz)
-    az = nz + 2 * R
-    outs = []
-    for fusion in (False, True):
-        c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k,
-                             rate_bits=rate, mode="swb", store="device", fusion=fusion)
-        pl = oocs.Plan(c)
-        load_fields(pl, vel, p0)
-        pl.run(2 * k)
-        outs.append([pl.read_raw(a, 0, az) for a in (1, 2)])
-        pl.close()
-    for a in range(2):
-        assert np.array_equal(outs[0][a], outs[1][a]), (a, np.flatnonzero(outs[0][a] != outs[1][a])[:8])
-
-
 @pytest.mark.parametrize("codec,rate", [("blockquant", 16), ("blockquant", 8), ("zfp", 12), ("trunc16", 16),
                                         ("identity", 32)])
-@pytest.mark.parametrize("fusion", [False, True])
-def test_decoded_velocity_is_bitwise_identical(codec, rate, fusion):
+def test_decoded_velocity_is_bitwise_identical(codec, rate):
     """OOCS_FLAG_DECODED_VELOCITY (device store): the stencil reads the velocity from a resident array
     decoded once at load instead of from each chunk's decode -- the same decode of the same records, so
     S_T is bitwise the same; reloading the velocity (load and write_raw) re-decodes it."""
-    if fusion and codec != "blockquant":
-        pytest.skip("fusion is BlockQuant-only")
     nx, ny, nz, n, k = 44, 36, 96, 4, 3
     vel, p0 = synth.fields(nx, ny, nz)
     vel2 = np.ascontiguousarray(vel[:, :, ::-1] * np.float32(0.9))
@@ -440,7 +417,7 @@ def test_decoded_velocity_is_bitwise_identical(codec, rate, fusion):
     outs = []
     for dec in (False, True):
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=n, tb_depth=k, codec=codec,
-                             rate_bits=rate, mode="swb", store="device", fusion=fusion, decoded_velocity=dec)
+                             rate_bits=rate, mode="swb", store="device", decoded_velocity=dec)
         pl = oocs.Plan(c)
         load_fields(pl, vel, p0)
         pl.run(2 * k)

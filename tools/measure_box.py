@@ -48,6 +48,30 @@ import numpy as np
 a = np.ones(1 << 28, dtype=np.float32); b = np.empty_like(a)
 t = time.perf_counter(); np.copyto(b, a); dt = time.perf_counter() - t
 out["host_memcpy_1thread_gbs"] = 2 * a.nbytes / dt / 1e9
+# multi-threaded host copy bandwidth (the 8-GPU bound needs host DRAM bandwidth; numpy's
+# copy releases the GIL, every thread copies its own 512 MiB pair of buffers), and the same while the GPU
+# streams duplex over PCIe (the DMA engines read and write the same DRAM)
+import threading
+def mt_copy(nthreads, secs=1.0):
+    bufs = [(np.ones(1 << 27, dtype=np.float32), np.empty(1 << 27, dtype=np.float32)) for _ in range(nthreads)]
+    done = [0] * nthreads
+    def worker(i):
+        a_, b_ = bufs[i]
+        t_end = time.perf_counter() + secs
+        while time.perf_counter() < t_end:
+            np.copyto(b_, a_)
+            done[i] += 1
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(nthreads)]
+    t0 = time.perf_counter()
+    for t_ in ths: t_.start()
+    for t_ in ths: t_.join()
+    el = time.perf_counter() - t0
+    return sum(done) * 2 * bufs[0][0].nbytes / el / 1e9
+out["host_memcpy_gbs_by_threads"] = {n_: mt_copy(n_) for n_ in (1, 2, 4, 8, out["cores_affinity"])}
+try:
+    out["numa_nodes"] = sorted(os.listdir("/sys/devices/system/node"))
+except Exception as e:
+    out["numa_nodes"] = str(e)
 print(json.dumps(out, indent=1))
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/measure_box.json", "w"), indent=1)

@@ -14,7 +14,7 @@ codec = sys.argv[sys.argv.index("--codec") + 1] if "--codec" in sys.argv else "b
 if codec == "trunc16":
     rate = 16
 c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, rate_bits=rate,
-                     mode="swb", store="device", codec=codec, fusion="--fuse" in sys.argv)
+                     mode="swb", store="device", codec=codec)
 pl = oocs.Plan(c)
 bench.load_state(pl, nx, ny, nz, 0)
 pl.run(k)

@@ -15,12 +15,12 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HOT = {
-    "stencil_step_tma_kernel<16, 0>": r"stencil_step_tma_kernelILi16ELi0E",
+    "stencil_step_tma_kernel<16>": r"stencil_step_tma_kernelILi16EE",
+    "star7_step_kernel": r"star7_step_kernel",
     "bq_encode_kernel<false, 15>": r"bq_encode_kernelILb0ELi15E",
     "bq_decode_kernel<false, 15>": r"bq_decode_kernelILb0ELi15E",
     "bq_encode_kernel<false, 7>": r"bq_encode_kernelILb0ELi7E",
     "bq_decode_kernel<false, 7>": r"bq_decode_kernelILb0ELi7E",
-    "stencil_step2_kernel": r"stencil_step2_kernel",
 }
 
 

@@ -70,6 +70,7 @@ def main():
                     help="host dispatcher (default) or stream replay: one stream per lane (Alg. 1 literal) / "
                          "copy + kernel stream per lane")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"])
+    ap.add_argument("--lanes", type=int, default=0, help="pipeline lanes (0 = 3, Alg. 1's strm[0:3])")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_timeline_c2.json"))
     a = ap.parse_args()
     nx, ny, nz, nb, k, T, rate = bench.WORKLOADS[a.workload]
@@ -77,7 +78,7 @@ def main():
         rate = 16
     cfg = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, codec=a.codec,
                            rate_bits=rate, mode="swb", store=a.store, resident_velocity=a.resident_velocity,
-                           schedule=a.schedule, timeline=True,
+                           schedule=a.schedule, timeline=True, n_lanes=a.lanes,
                            executor=a.executor)
     pl = oocs.Plan(cfg)
     bench.load_state(pl, nx, ny, nz, 0)
@@ -101,7 +102,7 @@ def main():
     res = {
         "workload": f"{a.workload}: {nx}x{ny}x{nz}, {nb} chunks, k={k}, T={T}, {a.codec} rate {rate}, swb, "
                     f"{a.store} store{', resident velocity' if a.resident_velocity else ''}, schedule {a.schedule}, "
-                    f"executor {a.executor}",
+                    f"executor {a.executor}, lanes {a.lanes or 3}",
         "wall_ms": wall,
         "gcell_updates_per_s": st.cell_updates / (wall * 1e-3) / 1e9,
         "bytes_h2d": st.bytes_h2d, "bytes_d2h": st.bytes_d2h,
