@@ -5,13 +5,18 @@ import json
 import sys
 
 
-def main(path, out, command, per_step=None):
+def main(path, out, command, per_step=None, window=None):
+    """window = "start:end" launch indices of the timed step (else the last per_step launches)."""
     rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
     hdr = rows[0]
     ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
     launches = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", "")) / 1e3)
                 for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
-    tail = launches[-per_step:] if per_step else launches
+    if window:
+        a, b = (int(x) for x in window.split(":"))
+        tail = launches[a:b]
+    else:
+        tail = launches[-per_step:] if per_step else launches
     share = {}
     for name, us in tail:
         base = name.split("<")[0]
@@ -28,4 +33,5 @@ def main(path, out, command, per_step=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else None)
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4] else None,
+         sys.argv[5] if len(sys.argv) > 5 else None)

@@ -2,6 +2,8 @@
 tools/gpu_final.sh: DRAM bytes vs algorithmic bytes of the same launch, per kernel.
 
 usage: python tools/make_ncu_summary.py STEP.ncu-rep DECODE.ncu-rep ENCODE.ncu-rep STEP_PLANES
+   or: python tools/make_ncu_summary.py --chunk CHUNK.ncu-rep   (one capture of an interior c2 chunk's six
+       launches, tools/gpu_round2.sh: decode, steps 1-4 (152/144/136/128 planes), encode)
 Algorithmic bytes: stencil 16 B per cell-update (STEP_PLANES x 1024^2); codec (r/8 + 4) B per value,
 values = 4 * grid.z planes x 1032^2 (grid z = array x slab)."""
 import json
@@ -14,8 +16,8 @@ RATE = 16
 AX = 1032
 
 
-def entry(rep, alg, unit):
-    e = summarise(rep)[0]
+def entry(rep, alg, unit, idx=0):
+    e = summarise(rep)[idx]
     e["alg_bytes_per_launch"] = alg
     e["alg_unit"] = unit
     e["dram_bytes_per_launch"] = e["dram_bytes"]
@@ -27,17 +29,23 @@ def entry(rep, alg, unit):
                               "inst_executed", "registers", "top_stalls", "source") if k in e}
 
 
-def codec_values(rep):
-    gz = int(summarise(rep)[0]["grid"].strip("()").split(",")[2])
+def codec_values(rep, idx=0):
+    gz = int(summarise(rep)[idx]["grid"].strip("()").split(",")[2])
     return 4 * gz * AX * AX, 4 * gz
 
 
 if __name__ == "__main__":
-    step, dec, enc, planes = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
-    out = {"step": entry(step, planes * 1024 * 1024 * 16, f"{planes} planes x 1024^2 cell-updates x 16 B")}
+    if sys.argv[1] == "--chunk":
+        rep = sys.argv[2]
+        step, dec, enc, planes, idx = rep, rep, rep, 152, {"step": 1, "decode": 0, "encode": 5}
+    else:
+        step, dec, enc, planes = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+        idx = {"step": 0, "decode": 0, "encode": 0}
+    out = {"step": entry(step, planes * 1024 * 1024 * 16, f"{planes} planes x 1024^2 cell-updates x 16 B", idx["step"])}
     for name, rep in (("decode", dec), ("encode", enc)):
-        v, pl = codec_values(rep)
-        out[name] = entry(rep, v * (RATE // 8 + 4), f"{pl} array-planes x {AX}^2 values x ({RATE // 8} + 4) B")
+        v, pl = codec_values(rep, idx[name])
+        out[name] = entry(rep, v * (RATE // 8 + 4), f"{pl} array-planes x {AX}^2 values x ({RATE // 8} + 4) B",
+                          idx[name])
     json.dump(out, open("profiles/ncu_summary.json", "w"), indent=1)
     print(json.dumps({k: {x: v.get(x) for x in ("duration_us", "traffic_over_alg", "alg_gbs", "issue_active_pct")}
                       for k, v in out.items()}, indent=1))
