@@ -1211,7 +1211,7 @@ __global__ void __launch_bounds__(256) peer_copy_kernel(const V *__restrict__ s0
 }
 
 cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, void *dst1, uint64_t bytes,
-                             cudaStream_t st) {
+                             cudaStream_t st, int ranges) {
     if (!bytes) return cudaSuccess;
     const uintptr_t all = reinterpret_cast<uintptr_t>(src0) | reinterpret_cast<uintptr_t>(dst0) |
                           reinterpret_cast<uintptr_t>(src1) | reinterpret_cast<uintptr_t>(dst1) | (uintptr_t)bytes;
@@ -1219,7 +1219,7 @@ cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, voi
     const bool v16 = (all & 15) == 0;
     const uint64_t n = bytes / (v16 ? 16 : 8);
     const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(148, (n + 1023) / 1024));
-    const dim3 grid(gx, 2);
+    const dim3 grid(gx, ranges == 1 ? 1 : 2);
     if (v16)
         peer_copy_kernel<uint4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(src0), static_cast<uint4 *>(dst0),
                                                        static_cast<const uint4 *>(src1), static_cast<uint4 *>(dst1), n);

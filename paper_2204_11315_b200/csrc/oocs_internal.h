@@ -54,9 +54,10 @@ cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int6
 // atomicMax; NaN compares above +Inf); *out must be initialised by the caller
 cudaError_t launch_absmax(const float *src, int64_t rows, int64_t n, int64_t pitch, uint32_t *out, cudaStream_t st);
 
-// multi-GPU halo send: two equal-length byte ranges (8-byte multiples), dst possibly peer memory
+// SM copy of one or two equal-length byte ranges (8-byte multiples), dst possibly peer memory: the multi-GPU
+// halo send, and the carry of region sharing (a copy-engine D2D of ~0.8 GB took 5.5 ms at c3)
 cudaError_t launch_peer_copy(const void *src0, void *dst0, const void *src1, void *dst1, uint64_t bytes,
-                             cudaStream_t st);
+                             cudaStream_t st, int ranges = 2);
 
 void set_error(const std::string &msg);
 

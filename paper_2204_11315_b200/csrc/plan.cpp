@@ -247,18 +247,42 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
         const oocs_block &b = geo.blocks[blk];
         const bool carry = i > 0 && b.carry_hi > b.carry_lo;
-        if (carry) {  // region sharing: the overlap is copied GPU-side from the previous chunk's buffer
-            E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_H2D, g - 1);
-            E.emit(OOCS_OP_CARRY, s, g, blk, t);
-            E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_CARRY, g);
+        // H2D(g) depends only on its stream's own earlier work (the D2H that emptied hf_buf[s], L chunks
+        // back) and the cross-sweep RAW waits, so the H2D engine can queue it while chunk g-1 is still in
+        // flight.  Algorithm 1 lists the previous chunk's compress / record / transfer first,
+        // on another stream: per-stream programs and events are unchanged.  Exception: when H2D(g) reads
+        // host planes that the pending chunk g-1's D2H writes (a cross-sweep RAW with one or two chunks per
+        // sweep), that D2H's record must precede the wait, so the tail goes first.
+        bool raw_on_pending = false;
+        if (pending >= 0 && g / nb > 0 && pending / nb == g / nb - 1) {
+            const oocs_block &pb = geo.blocks[blk_of(pending)];
+            raw_on_pending = pb.own_lo < b.body_hi && b.body_lo < pb.own_hi;
+        }
+        auto h2d = [&] {
+            raw_waits(g, b.body_lo, b.body_hi);
+            E.emit(OOCS_OP_H2D, s, g, blk, t);
+            E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_H2D, g);
+        };
+        if (!raw_on_pending) h2d();
+        if (carry) {
+            // region sharing: the overlap is copied GPU-side out of chunk g-1's buffer, on chunk g-1's
+            // stream (after its H2D and steps, before its encode overwrites the buffer: stream order),
+            // into hf_buf[s(g)] once chunk g-L's D2H has emptied it.  Not on stream s(g) ahead of H2D(g):
+            // that made every H2D wait for the previous chunk's carry (measured: 5.5 ms per chunk idle on
+            // the binding PCIe direction at c3 with a copy-engine carry)
+            const int sp = lane(g - 1);
+            // (when 2kR > W the source planes include planes carried into chunk g-1 by its own carry copy:
+            // ordered too, since chunk g-1's decode, earlier on this stream, waited for that copy)
+            if (g >= L) E.emit(OOCS_OP_WAIT, sp, g, blk, t, OOCS_EV_D2H, g - L);
+            E.emit(OOCS_OP_CARRY, sp, g, blk, t);
+            E.emit(OOCS_OP_RECORD, sp, g, blk, t, OOCS_EV_CARRY, g);
         }
         if (pending >= 0) {
-            tail(pending, carry ? g : -1);
+            tail(pending, -1);
             pending = -1;
         }
-        raw_waits(g, b.body_lo, b.body_hi);
-        E.emit(OOCS_OP_H2D, s, g, blk, t);
-        E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_H2D, g);
+        if (raw_on_pending) h2d();
+        if (carry) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_CARRY, g);
         if (g >= geo.n_ws) E.emit(OOCS_OP_WAIT, s, g, blk, t, OOCS_EV_ENC, g - geo.n_ws);
         E.emit(OOCS_OP_DECODE, s, g, blk, t);
         E.emit(OOCS_OP_RECORD, s, g, blk, t, OOCS_EV_DEC, g);

@@ -633,16 +633,23 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         if (g.cfg.mode == OOCS_MODE_BASELINE) {
             // lane of o is the previous chunk's lane; destination is chunk g's working set
             const int wprev = (int)((o.g - 1) % g.n_ws);
-            for (int a = 0; a < N_ARRAYS; ++a)
-                CU(cudaMemcpyAsync(wsa(p, w, a) + dst_off * g.pstride, wsa(p, wprev, a) + src_off * g.pstride,
-                                   (size_t)nplanes * g.pstride * 4, cudaMemcpyDeviceToDevice, st));
+            const uint64_t nb = (uint64_t)nplanes * g.pstride * 4;
+            auto sa = [&](int a) { return wsa(p, wprev, a) + src_off * g.pstride; };
+            auto da = [&](int a) { return wsa(p, w, a) + dst_off * g.pstride; };
+            CU(launch_peer_copy(sa(0), da(0), sa(1), da(1), nb, st));
+            CU(launch_peer_copy(sa(2), da(2), nullptr, nullptr, nb, st, 1));
             if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
         } else {
             const int sp = (int)((o.g - 1) % g.lanes);
-            for (int a = p->resident_vel ? 1 : 0; a < N_ARRAYS; ++a)
-                CU(cudaMemcpyAsync(p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB,
-                                   p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB, nplanes * PB,
-                                   cudaMemcpyDeviceToDevice, st));
+            auto sa = [&](int a) { return p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB; };
+            auto da = [&](int a) { return p->hf[s] + ((uint64_t)a * g.max_ext + dst_off) * PB; };
+            const uint64_t nb = (uint64_t)nplanes * PB;
+            if (p->resident_vel) {
+                CU(launch_peer_copy(sa(1), da(1), sa(2), da(2), nb, st));
+            } else {
+                CU(launch_peer_copy(sa(0), da(0), sa(1), da(1), nb, st));
+                CU(launch_peer_copy(sa(2), da(2), nullptr, nullptr, nb, st, 1));
+            }
             if (stats) stats->bytes_d2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
         }
         break;
@@ -776,9 +783,10 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
     return OOCS_OK;
 }
 
-// SEND is a kernel-stream op too: a peer copy kernel plus stream memory operations
+// SEND and CARRY are kernel-stream ops too: SM copy kernels (SEND plus stream memory operations)
 static bool is_kernel_op(int k) {
-    return k == OOCS_OP_DECODE || k == OOCS_OP_STEP || k == OOCS_OP_ENCODE || k == OOCS_OP_SEND;
+    return k == OOCS_OP_DECODE || k == OOCS_OP_STEP || k == OOCS_OP_ENCODE || k == OOCS_OP_SEND ||
+           k == OOCS_OP_CARRY;
 }
 static bool is_work_op(int k) { return k != OOCS_OP_WAIT && k != OOCS_OP_RECORD; }
 
@@ -936,8 +944,7 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
         switch (o.kind) {
         case OOCS_OP_H2D: return p->cstream[0];
         case OOCS_OP_D2H: return p->cstream[1];
-        case OOCS_OP_CARRY: return p->cstream[2];
-        default: return p->klanes[o.lane];
+        default: return p->klanes[o.lane];  // kernels, and the SM-copy CARRY / SEND
         }
     };
     std::vector<char> issued(n, 0), done(n, 0);
