@@ -214,10 +214,14 @@ def load_state(plan, nx, ny, nz_global, device):
         del v, p
 
 
-def copy_state(src, dst):
+def copy_state(src, dst, slab=128):
+    """Raw compressed state from one plan's store to another's, `slab` planes at a time (bounded host
+    memory: eight ranks of one node copy at once)."""
     a_lo, a_hi = src.info.store_lo + R, src.info.store_hi + R
     for a in range(3):
-        dst.write_raw(a, src.read_raw(a, a_lo, a_hi), a_lo, a_hi)
+        for z0 in range(a_lo, a_hi, slab):
+            z1 = min(a_hi, z0 + slab)
+            dst.write_raw(a, src.read_raw(a, z0, z1), z0, z1)
 
 
 def step_summary(stats_list):

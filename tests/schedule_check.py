@@ -52,19 +52,23 @@ def footprint(op, blocks, geo):
     # one half-size buffer per lane (hf_buf[s]), in plane units: incoming array a at
     # [a*ME, a*ME + E), outgoing owned planes of pressure j at [j*MO, j*MO + W)
     ME, MO = geo["max_ext"], geo["max_own"]
+    # OOCS_FLAG_RESIDENT_VELOCITY: the velocity never passes through the staging buffers (its compressed
+    # planes stay in HBM, read-only, and the decode reads them there)
+    a0 = 1 if geo.get("resident_velocity") else 0
     if kind == "H2D":
-        for a in range(3):
+        for a in range(a0, 3):
             out.append((("host", a), body_lo, body_hi, False))
             out.append((("hf", s), a * ME + body_lo - ext_lo, a * ME + ext_hi - ext_lo, True))
     elif kind == "CARRY":
         pb = blocks[op["block"] - 1]
         sp = (g - 1) % L
-        for a in range(3):
+        for a in range(a0, 3):
             out.append((("hf", sp), a * ME + c_lo - pb[2], a * ME + c_hi - pb[2], False))
             out.append((("hf", s), a * ME + c_lo - ext_lo, a * ME + c_hi - ext_lo, True))
     elif kind == "DECODE":
         for a in range(3):
-            out.append((("hf", s), a * ME, a * ME + E, False))
+            if a >= a0:
+                out.append((("hf", s), a * ME, a * ME + E, False))
             out.append((("ws", w, a), 0, E, True))
     elif kind == "STEP":
         st = op["arg"]

@@ -98,7 +98,8 @@ def _geo(c, blocks):
     L = c.n_lanes or 3
     n_ws = {0: L, 1: L, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
     return dict(k=c.tb_depth, n_ws=n_ws, lanes=L, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz,
-                max_ext=max(b[3] - b[2] for b in blocks), max_own=max(b[1] - b[0] for b in blocks))
+                max_ext=max(b[3] - b[2] for b in blocks), max_own=max(b[1] - b[0] for b in blocks),
+                resident_velocity=bool(c.flags & oocs.FLAG_RESIDENT_VELOCITY))
 
 
 def _check(c, steps):
@@ -340,3 +341,36 @@ def test_multirank_exchange_region_accounting():
                                                                       one.staging_bytes)
     slot = _al(4 * oocs.R * b.plane_bytes)
     assert b.arena_bytes - one.arena_bytes == _al(256 + 8 * slot)
+
+
+def test_schedule_race_free_random_configs():
+    """Seeded random configurations beyond the grid above (chunk counts with remainders, 2kR > W, up to 8
+    lanes, resident velocity, 2-4 sweeps): every lowered schedule is race-free under stream + event
+    semantics, and every chunk is decoded, stepped and encoded exactly once per sweep."""
+    rng = np.random.default_rng(2204)
+    done = 0
+    while done < 60:
+        n = int(rng.integers(1, 13))
+        k = int(rng.integers(1, 5))
+        units = int(rng.integers(n, 4 * n + 6))
+        nz = 4 * units
+        mode = ["swb", "dwb", "compress", "baseline"][int(rng.integers(0, 4))]
+        codec = "identity" if mode == "baseline" else ["blockquant", "zfp", "trunc16"][int(rng.integers(0, 3))]
+        rate = {"identity": 32, "blockquant": 16, "zfp": 12, "trunc16": 16}[codec]
+        lanes = [0, 2, 4, 8][int(rng.integers(0, 4))]
+        sched = ["alg1", "dag", "dag_func"][int(rng.integers(0, 3))]
+        resv = mode != "baseline" and bool(rng.integers(0, 2))
+        c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, codec=codec, rate_bits=rate, n_lanes=lanes,
+                schedule=sched, resident_velocity=resv)
+        try:
+            oocs.oocs_plan_table(c)
+        except oocs.OocsError:
+            continue  # k*R >= W for some chunk: rejected, not a schedule
+        sweeps = int(rng.integers(2, 5))
+        ops, bad = _check(c, sweeps * k)
+        assert bad == [], (n, k, nz, mode, codec, lanes, sched, resv, bad[:3])
+        for kind, per in (("DECODE", 1), ("STEP", k), ("ENCODE", 1)):
+            if mode == "baseline" and kind != "STEP":
+                continue
+            assert sum(o["kind"] == kind for o in ops) == sweeps * n * per
+        done += 1

@@ -156,7 +156,7 @@ def test_ext_streams_order_and_results():
     want = ref.read_raw(2, 0, az)
     ref.close()
     streams = [torch.cuda.Stream() for _ in range(3)]
-    for executor in ("dispatch", "single"):
+    for executor in ("dispatch", "single", "split"):
         pl = _plan(nx, ny, nz, n, k, codec="blockquant", executor=executor,
                    ext_streams=[s.cuda_stream for s in streams])
         load_fields(pl, vel, p0)
@@ -173,3 +173,41 @@ def test_ext_streams_order_and_results():
         pl.close()
     for s in streams:  # the plan did not destroy the caller's streams
         s.synchronize()
+
+
+def test_cfl_check_at_load_device():
+    nx, ny, nz = 32, 16, 32
+    vel, p0 = synth.fields(nx, ny, nz)
+    az = vel.shape[0]
+    bad_dt = 1.01 * (2 / (3 * 2048 / 315) ** 0.5) / float(np.abs(vel).max())
+    pl = oocs.Plan(oocs.make_config(nx=nx, ny=ny, nz=nz, dt=bad_dt, n_blocks=2, tb_depth=1, mode="swb",
+                                    store="device"))
+    tv = torch.from_numpy(vel).cuda()
+    with pytest.raises(oocs.OocsError) as e:
+        pl.load_device(0, tv, 0, az)
+    assert e.value.status == 2
+    pl.load_device(1, torch.from_numpy(p0).cuda(), 0, az)
+    pl.close()
+
+
+@pytest.mark.parametrize("codec,rate", [("zfp", 12), ("trunc16", 16)])
+def test_star7_other_codecs_pipeline_vs_oracle(codec, rate):
+    """STAR7 through the ZFP / Truncate-16 pipelines: the GPU's S_T against the oracle pipeline's (same
+    codec, same stencil) within the codec's own error after one sweep."""
+    nx, ny, nz, n, k = 44, 20, 48, 3, 2
+    vel, p0 = synth.fields(nx, ny, nz)
+    az, ay, ax = p0.shape
+    dt = synth.dt_for()
+    cid, prm = {"zfp": (2, rate), "trunc16": (3, 0)}[codec]
+    S = [oracle.encode_planes(a, cid, prm) for a in (vel, p0, p0)]
+    pl = _plan(nx, ny, nz, n, k, codec=codec, rate=rate, stencil="star7")
+    for a in range(3):
+        pl.write_raw(a, S[a], 0, az)
+    pl.run(k)
+    got = pl.store(2, 0, az).astype(np.float64)
+    pl.close()
+    oracle.pipeline(ax, ay, nz, n, k, dt, k, cid, prm, *S, stencil=oracle.STENCIL_STAR7)
+    want = oracle.decode_planes(S[2], ax, ay, az, cid, prm).astype(np.float64)
+    amax = np.abs(want).max()
+    tol = (2e-3 if codec == "zfp" else 2 ** -7) * amax
+    assert np.max(np.abs(got - want)) <= tol

@@ -1,6 +1,6 @@
 """Small runs of every hot-path kernel and schedule for compute-sanitizer (memcheck / racecheck /
 synccheck): ragged grids, every codec, host and device stores, Alg. 1 and DAG schedules, the resident
-(compressed / decoded) velocity flags."""
+(compressed / decoded) velocity flags, both stencils, the BASELINE mode (its carry is an SM copy too)."""
 import os
 import sys
 
@@ -18,7 +18,10 @@ for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("trunc
     for store, sched, mode, extra in (("host", "alg1", "swb", {}), ("device", "alg1", "swb", {}),
                                       ("host", "dag_func", "dwb", {}),
                                       ("device", "alg1", "swb", {"decoded_velocity": True}),
-                                      ("host", "alg1", "swb", {"resident_velocity": True})):
+                                      ("host", "alg1", "swb", {"resident_velocity": True}),
+                                      ("host", "alg1", "compress", {"stencil": "star7"}),
+                                      ("host", "alg1", "baseline", {}) if codec == "identity" else
+                                      ("device", "alg1", "dwb", {"stencil": "star7"})):
         c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=3, tb_depth=2, codec=codec,
                              rate_bits=rate, mode=mode, store=store, schedule=sched, **extra)
         pl = oocs.Plan(c)
