@@ -232,7 +232,7 @@ def step_summary(stats_list):
 
 def agg(stats_list):
     out = {"ms": sum(s.wall_ms for s in stats_list), "kernel_ms": [0.0] * 3, "launches": [0] * 3,
-           "alg": [0] * 3, "h2d": 0, "d2h": 0, "cells": 0, "computed": 0, "exch": 0}
+           "alg": [0] * 3, "h2d": 0, "d2h": 0, "cells": 0, "computed": 0, "exch": 0, "copy_launches": 0}
     for s in stats_list:
         for i in range(3):
             out["kernel_ms"][i] += s.kernel_ms[i]
@@ -243,6 +243,7 @@ def agg(stats_list):
         out["cells"] += s.cell_updates
         out["computed"] += s.cell_updates_computed
         out["exch"] += s.bytes_exchange
+        out["copy_launches"] += s.copy_launches
     return out
 
 
@@ -546,7 +547,7 @@ def main():
                 "per_kernel": {names[i]: {"ms": a["kernel_ms"][i], "launches": a["launches"][i],
                                           "GBps": (a["alg"][i] / (a["kernel_ms"][i] * 1e-3) / 1e9)
                                           if a["kernel_ms"][i] else None} for i in range(3)}}
-    gpu_launches = int(sum(a["launches"]))
+    gpu_launches = int(sum(a["launches"]) + a["copy_launches"])  # codec / stencil kernels + SM carry copies
     # PCIe roofline of the pipeline: per useful cell-update it must move h2d_pc bytes in and d2h_pc out;
     # time >= max(in/B_h2d, out/B_d2h, (in+out)/B_duplex) on the link measured live on this box
     mb = pcie_live
@@ -588,6 +589,7 @@ def main():
     # ---- variant: compressed state resident in HBM (NEXT-2), kernels only ----------------------------
     value_dev = None
     if not args.no_device_resident:
+        torch.cuda.empty_cache()  # the synthetic generator's cached blocks
         need = oocs.oocs_plan_estimate(oocs.make_config(
             nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=args.codec, rate_bits=rate,
             mode="swb", store="device", device=local, rank=rank, world=world)).arena_bytes

@@ -195,7 +195,7 @@ typedef struct {
     uint64_t cell_updates_computed; /* incl. redundant temporal-blocking halo updates */
     uint64_t alg_bytes[3];          /* algorithmic HBM bytes per kind */
     int32_t data_error;             /* 1 if the encoder saw NaN/Inf/|x|>=2^126 */
-    int32_t reserved;
+    int32_t copy_launches;          /* SM copy kernels launched: region-sharing carries, multi-GPU sends */
     double busy_ms[4];              /* OOCS_FLAG_TIMELINE: busy time (union of op spans) of the H2D copies, the
                                      * D2H copies, the kernels and the exchange; 0 without the flag */
 } oocs_stats;

@@ -73,7 +73,7 @@ class PlanInfo(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("wall_ms", f64), ("kernel_ms", f64 * 3), ("kernel_launches", i64 * 3), ("bytes_h2d", u64),
                 ("bytes_d2h", u64), ("bytes_d2d", u64), ("bytes_exchange", u64), ("cell_updates", u64),
-                ("cell_updates_computed", u64), ("alg_bytes", u64 * 3), ("data_error", i32), ("reserved", i32),
+                ("cell_updates_computed", u64), ("alg_bytes", u64 * 3), ("data_error", i32), ("copy_launches", i32),
                 ("busy_ms", f64 * 4)]
 
     def as_dict(self):

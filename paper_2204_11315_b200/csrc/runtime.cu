@@ -638,7 +638,10 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
             auto da = [&](int a) { return wsa(p, w, a) + dst_off * g.pstride; };
             CU(launch_peer_copy(sa(0), da(0), sa(1), da(1), nb, st));
             CU(launch_peer_copy(sa(2), da(2), nullptr, nullptr, nb, st, 1));
-            if (stats) stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
+            if (stats) {
+                stats->bytes_d2d += (uint64_t)N_ARRAYS * nplanes * g.ax * g.ay * 4;
+                stats->copy_launches += 2;
+            }
         } else {
             const int sp = (int)((o.g - 1) % g.lanes);
             auto sa = [&](int a) { return p->hf[sp] + ((uint64_t)a * g.max_ext + src_off) * PB; };
@@ -650,6 +653,7 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
                 CU(launch_peer_copy(sa(0), da(0), sa(1), da(1), nb, st));
                 CU(launch_peer_copy(sa(2), da(2), nullptr, nullptr, nb, st, 1));
             }
+            if (stats) stats->copy_launches += p->resident_vel ? 1 : 2;
             if (stats) stats->bytes_d2d += (uint64_t)(N_ARRAYS - (p->resident_vel ? 1 : 0)) * nplanes * PB;
         }
         break;
@@ -771,6 +775,7 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
                 if (oocs_status r = wait_geq(st, &p->xflags[side ? F_FREE_HI : F_FREE_LO], t1 - 1)) return r;
             const int64_t off = side ? W - kR : 0;
             CU(launch_peer_copy(enc_out(0, off), pr.slot[par][0], enc_out(1, off), pr.slot[par][1], p->gh_bytes, st));
+            if (stats) stats->copy_launches++;
             if (oocs_status r = write_flag(st, pr.flags + (side ? F_READY_LO : F_READY_HI), t1)) return r;
             if (stats) stats->bytes_exchange += 2 * p->gh_bytes;
         }
