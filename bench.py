@@ -75,6 +75,10 @@ def parse():
     ap.add_argument("--no-compare", action="store_true", help="skip the uncompressed / memory comparison")
     ap.add_argument("--codec", default="blockquant", choices=["blockquant", "zfp", "trunc16"],
                     help="fixed-rate codec of the compressed state (ZFP = NEXT-1)")
+    # 2 lanes: the same throughput as Alg. 1's three streams on every workload (profiles/r02_lanes.json:
+    # c3 33.01 vs 33.01) with one half-size staging buffer less, -20% device memory
+    ap.add_argument("--lanes", type=int, default=2, help="pipeline lanes of the compressed modes (Alg. 1's strm[0:3] "
+                    "= 3; each lane owns one half-size staging buffer)")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
                     help="stream/event schedule of the host-store pipeline (e2e)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -382,11 +386,12 @@ def main():
         nz, nblocks = nzr * world, nbr * world
         workload = (f"{args.workload}: {nx}x{ny}x{nz} fp32 interior (+4-cell halo), {nblocks} z-chunks, {T} steps "
                     f"per step, temporal depth k={k}, {CODEC_NAME[args.codec]} rate {rate} bits/value, single "
-                    f"working buffer, compressed state in pinned host memory (out-of-core, PCIe in the timed region)")
+                    f"working buffer, {args.lanes} pipeline lanes, compressed state in pinned host memory "
+                    f"(out-of-core, PCIe in the timed region)")
         raw_gb = 3 * (nx + 2 * R) * (ny + 2 * R) * (nzr + 2 * R) * 4 / 1e9
         config = {"workload": workload, "nx": nx, "ny": ny, "nz": nz, "n_blocks": nblocks, "tb_depth": k,
                   "time_steps_per_step": T, "rate_bits": rate, "codec": args.codec, "mode": "swb",
-                  "store": "pinned host", "raw_state_gb_per_gpu": raw_gb,
+                  "store": "pinned host", "raw_state_gb_per_gpu": raw_gb, "lanes": args.lanes,
                   "parallelism": f"z-slabs x{world}",
                   "l2": f"inputs larger than L2 (compressed state {3 * nx * ny * nzr * rate / 8 / 1e9:.1f} GB/GPU "
                         ">> 126 MB, streamed over PCIe every step), no flush needed"}
@@ -461,7 +466,7 @@ def main():
                              rate_bits=rate if codec != "identity" else 32, mode=mode, store=store, device=local,
                              rank=rank if wl is None else 0, world=world if wl is None else 1,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
-                             decoded_velocity=decoded_velocity)
+                             decoded_velocity=decoded_velocity, n_lanes=0 if mode == "baseline" else args.lanes)
         pl = oocs.Plan(c)
         if world > 1 and wl is None:
             odist.connect(pl, gloo=gloo)
@@ -472,7 +477,7 @@ def main():
     # ---- the out-of-core plan: compressed state in pinned host memory ------------------------------
     est = oocs.oocs_plan_estimate(oocs.make_config(
         nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=args.codec, rate_bits=rate, mode="swb",
-        store="host", device=local, rank=rank, world=world))
+        store="host", device=local, rank=rank, world=world, n_lanes=args.lanes))
     avail = host_mem_available()
     local_ranks = env_int("LOCAL_WORLD_SIZE", world)
     if avail is not None and est.store_bytes * local_ranks > 0.8 * avail and nbr > 1:
@@ -490,7 +495,7 @@ def main():
                   file=sys.stderr)
             est = oocs.oocs_plan_estimate(oocs.make_config(
                 nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nblocks, tb_depth=k, codec=args.codec, rate_bits=rate,
-                mode="swb", store="host", device=local, rank=rank, world=world))
+                mode="swb", store="host", device=local, rank=rank, world=world, n_lanes=args.lanes))
     if avail is not None and est.store_bytes * local_ranks > 0.9 * avail:
         print(f"bench: the pinned host stores need {est.store_bytes * local_ranks / 1e9:.1f} GB, the host has "
               f"{avail / 1e9:.1f} GB available", file=sys.stderr)
@@ -640,12 +645,17 @@ def main():
                                       codec="identity" if base_mode else args.codec, rate_bits=32 if base_mode else rate,
                                       mode=mode, store="host", device=local)
                 mem.setdefault(wname, {})[mode] = oocs.oocs_plan_estimate(cc).arena_bytes / 1e9
+            cc = oocs.make_config(nx=wx, ny=wy, nz=wz, dt=dt, n_blocks=wb, tb_depth=k, codec=args.codec,
+                                  rate_bits=rate, mode="swb", store="host", device=local, n_lanes=2)
+            mem[wname]["swb_2_lanes"] = oocs.oocs_plan_estimate(cc).arena_bytes / 1e9
         compare = {"workload": f"c2 (configs[1]): {cnx}x{cny}x{cnz}, {cnb} chunks, k={ck}, T={cT}",
                    "compressed_e2e": runs["compressed_swb"]["value"],
                    "uncompressed_baseline_e2e": runs["uncompressed_baseline"]["value"],
                    "speedup_compressed_vs_uncompressed": runs["compressed_swb"]["value"] / runs["uncompressed_baseline"]["value"],
                    "paper_speedup_v100": 1.1, "peak_gpu_mem_gb_by_mode": mem,
                    "mem_reduction_swb_vs_baseline": {w: 1 - m["swb"] / m["baseline"] for w, m in mem.items()},
+                   "mem_reduction_swb_2_lanes_vs_baseline": {w: 1 - m["swb_2_lanes"] / m["baseline"]
+                                                             for w, m in mem.items()},
                    "paper_mem_reduction_v100": 0.33}
 
     cpu = None
