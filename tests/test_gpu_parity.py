@@ -278,6 +278,7 @@ def test_lossy_modes_are_bitwise_identical(rate):
     # the same schedules replayed onto streams (one per lane, Alg. 1 literally / copy + kernel per lane)
     # instead of the host dispatcher
     variants += [v + (ex,) for ex in ("single", "split") for v in variants[:4] + variants[6:8]]
+    variants += [("swb", "host", False, 2, "alg1")]  # the bench's out-of-core configuration (2 lanes)
     for mode, store, resident, lanes, sched, *ex in variants:
         pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store, resident_velocity=resident,
                        n_lanes=lanes, schedule=sched, executor=ex[0] if ex else "dispatch")
