@@ -35,7 +35,8 @@ def plans(request):
     dt = float(synth.dt_for())
     codec = request.param
     mk = lambda store: oocs.Plan(oocs.make_config(nx=NX, ny=NY, nz=NZ, dt=dt, n_blocks=NB, tb_depth=K,
-                                                  rate_bits=RATE, mode="swb", store=store, codec=codec))
+                                                  rate_bits=RATE, mode="swb", store=store, codec=codec,
+                                                  n_lanes=2))  # bench.py --lanes 2
     dev = mk("device")
     bench.load_state(dev, NX, NY, NZ, 0)
     host = mk("host")

@@ -1,7 +1,8 @@
 """Parity at the configurations the bench quotes: BASELINE.json configs[2] (c3 = 2048^3, 16 chunks) at
 (k, r) = (4, 16) [the bench line], (8, 8) and (4, 24), and configs[3]'s per-GPU slab c4slab (4096^2 x 512,
 8 chunks of W = 64, kR/W = 1/4), in the launch configuration bench.py times (single working buffer,
-Algorithm 1, host dispatcher; pinned host store, and for (4, 16) also the HBM-resident store).
+Algorithm 1 over 2 lanes as bench.py runs it, host dispatcher; pinned host store, and for (4, 16) also the
+HBM-resident store).
 
 The oracle cannot run these grids, so it recomputes 256 sampled 4x4x4 output blocks one by one
 (decode, k steps, encode, in the paper's order).  To cover the cross-sweep hazards
@@ -131,7 +132,7 @@ def test_sampled_blocks_second_sweep(case, store):
     nbx, nby, nbz = ax // 4, ay // 4, az // 4
     dt = float(synth.dt_for())
     plan = oocs.Plan(oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nb, tb_depth=k, codec="blockquant",
-                                      rate_bits=rate, mode="swb", store=store))
+                                      rate_bits=rate, mode="swb", store=store, n_lanes=2))  # bench.py --lanes 2
     try:
         rng = np.random.default_rng(11315 + len(case))
         samples = _samples(nx, ny, nz, nb, k, rng)
