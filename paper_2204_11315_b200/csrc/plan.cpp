@@ -229,12 +229,11 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         return;
     }
     int64_t pending = -1;
-    // tail of chunk p on its lane; `carry_ev` >= 0: the next chunk's carry copy reads hf_buf[s(p)],
-    // which ENCODE(p) overwrites (one half-size buffer per stream for both directions, P:L146,
-    // P:L153-155), so ENCODE waits for that copy.
-    auto tail = [&](int64_t p, int64_t carry_ev) {
+    // tail of chunk p on its lane.  The next chunk's carry copy reads hf_buf[s(p)], which
+    // ENCODE(p) overwrites (one half-size buffer per stream for both directions): the carry is
+    // issued on this same stream before the tail, so stream order protects it.
+    auto tail = [&](int64_t p) {
         const int s = lane(p), blk = blk_of(p), t = (int)(p / nb);
-        if (carry_ev >= 0) E.emit(OOCS_OP_WAIT, s, p, blk, t, OOCS_EV_CARRY, carry_ev);
         E.emit(OOCS_OP_ENCODE, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_ENC, p);
         // multi-GPU: the edge planes go to the neighbour's ghost slot straight from the encoded buffer,
@@ -278,7 +277,7 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
             E.emit(OOCS_OP_RECORD, sp, g, blk, t, OOCS_EV_CARRY, g);
         }
         if (pending >= 0) {
-            tail(pending, -1);
+            tail(pending);
             pending = -1;
         }
         if (raw_on_pending) h2d();
@@ -289,7 +288,7 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         for (int st = 1; st <= geo.k; ++st) E.emit(OOCS_OP_STEP, s, g, blk, t, st);
         pending = g;
     }
-    if (pending >= 0) tail(pending, -1);  // drain epilogue
+    if (pending >= 0) tail(pending);  // drain epilogue
 }
 
 // ---------------------------------------------------------------------------
