@@ -199,3 +199,99 @@ def test_sampled_blocks_second_sweep(case, store):
         # per-element tolerance above is then the whole bar (the histogram is reported)
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("nx,ny", [(2048, 2048), (2040, 2044)])
+def test_full_plane_step_vs_oracle(nx, ny):
+    """One stencil step over whole c3-sized planes (2048^2, and a ragged 2040 x 2044 whose last CTA tiles
+    are partial) against the oracle, every cell: normwise <= 1e-6 (Q16) and the per-element ulp histogram
+    (written to $OOCS_REPORT_DIR/fullplane_ulp_<nx>x<ny>.json)."""
+    from test_gpu_parity import _rel_err, _ulp_distance, from_ws, stream, to_ws
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    nz = 24
+    vel, p0 = synth.fields(nx, ny, nz)
+    rng = np.random.default_rng(nx + ny)
+    pprev = (p0 * np.float32(0.97) + rng.normal(scale=1e-3, size=p0.shape).astype(np.float32)).astype(np.float32)
+    pprev[:R], pprev[-R:], pprev[:, :R], pprev[:, -R:], pprev[:, :, :R], pprev[:, :, -R:] = 0, 0, 0, 0, 0, 0
+    pprev = np.ascontiguousarray(pprev)
+    dt = synth.dt_for()
+    az, ay, ax = p0.shape
+    o = pprev.copy()
+    oracle.step(vel, o, p0, dt, R, az - R)
+    tv, tp, tc = to_ws(vel), to_ws(pprev), to_ws(p0)
+    oocs.oocs_step(tv.data_ptr(), tp.data_ptr(), tc.data_ptr(), ax, ay, az, oocs.pitch_for(ax), dt, R, az - R,
+                   stream())
+    torch.cuda.synchronize()
+    g = from_ws(tp, ax)
+    sl = (slice(R, az - R), slice(R, ay - R), slice(R, ax - R))
+    rel = _rel_err(g[sl], o[sl].astype(np.float64))
+    d = _ulp_distance(g[sl], o[sl]).ravel()
+    counts = np.histogram(d, bins=[0, 1, 2, 3, 5, 9, 17, 65, 1 << 62])[0].tolist()
+    rd = os.environ.get("OOCS_REPORT_DIR")
+    if rd:
+        os.makedirs(rd, exist_ok=True)
+        with open(os.path.join(rd, f"fullplane_ulp_{nx}x{ny}.json"), "w") as f:
+            json.dump({"cells": int(d.size), "bins_ulp": ["0", "1", "2", "3-4", "5-8", "9-16", "17-64", ">64"],
+                       "counts": counts, "median_ulp": float(np.median(d)), "p99_ulp": float(np.percentile(d, 99)),
+                       "max_ulp": int(d.max()), "normwise_rel_err": rel}, f, indent=1)
+    assert rel <= 1e-6
+    # untouched outside the updated region
+    assert np.array_equal(g[:R], pprev[:R]) and np.array_equal(g[:, :R], pprev[:, :R])
+    assert np.array_equal(g[:, :, ax - R:], pprev[:, :, ax - R:])
+
+
+def test_sampled_blocks_second_sweep_zfp():
+    """The paper's codec (ZFP fixed rate, NEXT-1) at c3 (2048^3, 16 chunks, k = 4, rate 12), two sweeps,
+    host store, 2 lanes: 256 sampled blocks of S_2 against the oracle's second sweep from the GPU's S_1
+    (ZFP records: 8 * rate bytes per 4x4x4 block, slab-major like BlockQuant's).  Per element within
+    twice the oracle's own ZFP round-trip error on the block plus the stencil's 1e-6 per step; bit-identical
+    records counted (ZFP's embedded planes carry the stencil's last-ulp differences, so fewer are)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    nx = ny = nz = 2048
+    nb, k, rate = 16, 4, 12
+    kR, rec = k * R, 8 * rate
+    ax, ay, az = nx + 2 * R, ny + 2 * R, nz + 2 * R
+    nbx, nby, nbz = ax // 4, ay // 4, az // 4
+    dt = float(synth.dt_for())
+    plan = oocs.Plan(oocs.make_config(nx=nx, ny=ny, nz=nz, dt=dt, n_blocks=nb, tb_depth=k, codec="zfp",
+                                      rate_bits=rate, mode="swb", store="host", n_lanes=2))
+    try:
+        samples = _samples(nx, ny, nz, nb, k, np.random.default_rng(2204))
+        zneed = sorted({z for (_, _, bz) in samples for z in range(max(0, bz - kR // 4), min(nbz, bz + kR // 4 + 1))})
+        bench.load_state(plan, nx, ny, nz, 0)
+        plan.run(k)
+        slab = lambda a, z: plan.read_raw(a, 4 * z, 4 * z + 4).reshape(nby, nbx, rec)[None]
+        S1 = [{z: slab(a, z) for z in zneed} for a in (1, 2)]
+        V = {z: slab(0, z) for z in zneed}
+        bench.load_state(plan, nx, ny, nz, 0)
+        st = plan.run(2 * k)
+        assert st.bytes_h2d == 2 * 3 * (nz + 2 * R) * plan.info.plane_bytes
+        out_slabs, exact, n = {}, 0, 0
+        for (bx, by, bz) in samples:
+            arrs, (x0, y0, z0), (sx, sy, sz) = _cone(S1, V, rec, nbx, nby, bx, by, bz, kR, nbz)
+            v, pp, pc = (oracle.decode_planes(a, sx, sy, sz, 2, rate) for a in arrs)
+            pp, pc = oracle.incore(v, pp, pc, dt, k)
+            lx, ly, lz = 4 * (bx - x0), 4 * (by - y0), 4 * (bz - z0)
+            for arr, want in ((1, pp), (2, pc)):
+                if (arr, bz) not in out_slabs:
+                    out_slabs[(arr, bz)] = plan.read_raw(arr, 4 * bz, 4 * bz + 4).reshape(nby, nbx, rec)
+                r = out_slabs[(arr, bz)][by, bx].tobytes()
+                blk = np.ascontiguousarray(want[lz:lz + 4, ly:ly + 4, lx:lx + 4]).reshape(64)
+                ref_rec = oracle.zfp_encode_block(blk, rate)
+                exact += r == ref_rec
+                n += 1
+                got = oracle.zfp_decode_block(r, rate).astype(np.float64)
+                ref = oracle.zfp_decode_block(ref_rec, rate).astype(np.float64)
+                amax = max(float(np.abs(blk).max()), 1e-30)
+                err = float(np.abs(ref - blk.astype(np.float64)).max())
+                tol = 2 * err + 4 * k * 1e-6 * amax + 4 * float(np.spacing(np.float32(amax)))
+                assert np.all(np.abs(got - blk.astype(np.float64)) <= tol), (bx, by, bz, arr)
+        rd = os.environ.get("OOCS_REPORT_DIR")
+        if rd:
+            os.makedirs(rd, exist_ok=True)
+            with open(os.path.join(rd, "fullsize_c3_zfp_k4_r12_host.json"), "w") as f:
+                json.dump({"case": "c3 zfp k4 r12", "records_compared": n, "records_bit_identical": exact}, f)
+    finally:
+        plan.close()
