@@ -523,7 +523,9 @@ def main():
         for _ in range(args.steps):
             per.append(host.run(T))
         barrier()
-    host_wall = time.perf_counter() - t0
+        # the host clock stops here: stopping the nvidia-smi sampler (it finishes its current query
+        # first, up to ~1 s) is not part of the K steps
+        host_wall = time.perf_counter() - t0
     a = agg(per)
     dev_ms = allmax(a["ms"])
     wall_ms = allmax(host_wall * 1e3)
