@@ -272,6 +272,14 @@ oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out);
 oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs_op *ops, int64_t cap,
                           int64_t *n_ops);
 
+/* The same for a run that starts after `first_sweep` sweeps of earlier runs of the same plan: with a
+ * host store, codec modes, Algorithm 1 and world == 1 ("chainable"), consecutive runs continue one
+ * global chunk counter (lanes, working sets, event instances) and the run's first cross-sweep waits name
+ * the previous run's write-backs -- what lets oocs_run_async issue a run while the previous one drains.
+ * Other configurations restart at chunk 0 (identical to oocs_schedule).  Errors: OOCS_ERR_CONFIG. */
+oocs_status oocs_schedule_at(const oocs_config *cfg, int64_t steps, int64_t first_sweep, oocs_op *ops,
+                             int64_t cap, int64_t *n_ops);
+
 /* What oocs_plan_create would allocate for cfg (arena = the device peak, pinned host store, working
  * sets, staging), without allocating anything: the paper's memory comparison for
  * configurations larger than this machine.  Errors: OOCS_ERR_CONFIG. */
@@ -366,6 +374,25 @@ oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src
  * Errors: OOCS_ERR_CONFIG (steps), OOCS_ERR_DATA (encoder rejected a value;
  * state undefined), OOCS_ERR_CUDA, OOCS_ERR_EXCHANGE (world > 1 and not connected), OOCS_ERR_STATE. */
 oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out);
+
+/* Issue `steps` steps and return once every operation is issued, without waiting for them (the run's
+ * tail -- the last chunk's kernels and write-back -- may still be in flight).  A following
+ * oocs_run_async on a chainable plan (host store, codec modes, OOCS_SCHED_ALG1, world == 1, host
+ * dispatcher, no OOCS_FLAG_TIMELINE) starts while that tail drains: its first H2D waits only for what
+ * it really depends on (the lane buffer's previous write-back, the previous sweep's write-back of the
+ * planes it reads -- oocs_schedule_at), which overlaps the two runs' pipeline drain and fill
+ * ("overlap the first H2D with the previous run's drain").  Otherwise it waits for the
+ * previous run first.  Every other call on the plan (load, store, raw I/O, timeline, destroy) completes
+ * the runs in flight first.  The result is bitwise that of the same steps in oocs_run calls.
+ * Errors: as oocs_run (a data error is reported by oocs_wait). */
+oocs_status oocs_run_async(oocs_plan *plan, int64_t steps);
+
+/* Complete every run in flight and return their stats in issue order: min(cap, n) entries into out,
+ * *n_runs = n (may be NULL).  A run's wall_ms counts from its start mark, which follows the previous
+ * run's end mark, so the wall times of a chain add up to the chain's device time.
+ * Errors: OOCS_ERR_CONFIG (cap < 0, or out NULL with cap > 0), OOCS_ERR_DATA, OOCS_ERR_CUDA,
+ * OOCS_ERR_EXCHANGE, OOCS_ERR_STATE. */
+oocs_status oocs_wait(oocs_plan *plan, oocs_stats *out, int64_t cap, int64_t *n_runs);
 
 /* Spans of the last oocs_run made with OOCS_FLAG_TIMELINE, in schedule order.  Copies min(cap, n)
  * spans into out (out may be NULL to query n); *n_spans = n (0 if the flag was not set).

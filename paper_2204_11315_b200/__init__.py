@@ -22,7 +22,7 @@ __all__ = [
     "R", "OOCS_OK", "OocsError", "Config", "Stats", "PlanInfo", "Block", "Op",
     "lib", "oocs_plan_table", "oocs_schedule", "oocs_encoded_bytes", "oocs_plan_create",
     "oocs_plan_query", "oocs_plan_estimate", "oocs_destroy", "oocs_load", "oocs_store", "oocs_load_device", "oocs_store_device", "oocs_store_read_raw",
-    "oocs_store_write_raw", "oocs_run", "oocs_decode", "oocs_encode", "oocs_step",
+    "oocs_store_write_raw", "oocs_run", "oocs_run_async", "oocs_wait", "oocs_decode", "oocs_encode", "oocs_step",
     "oocs_peer_handle", "oocs_peer_connect", "PEER_HANDLE_BYTES", "Plan", "XOFF", "pitch_for",
 ]
 
@@ -136,6 +136,9 @@ def lib():
             "oocs_store_read_raw": ([vp, i32, vp, i64, i64], i32),
             "oocs_store_write_raw": ([vp, i32, vp, i64, i64], i32),
             "oocs_run": ([vp, i64, P(Stats)], i32),
+            "oocs_run_async": ([vp, i64], i32),
+            "oocs_wait": ([vp, vp, i64, P(i64)], i32),
+            "oocs_schedule_at": ([P(Config), i64, i64, vp, i64, P(i64)], i32),
             "oocs_timeline": ([vp, vp, i64, P(i64)], i32),
             "oocs_decode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp], i32),
             "oocs_encode": ([vp, vp, i64, i64, i64, i64, i32, i32, vp, vp], i32),
@@ -199,11 +202,13 @@ def oocs_plan_table(cfg: Config):
     return [(b.own_lo, b.own_hi, b.ext_lo, b.ext_hi, b.carry_lo, b.carry_hi, b.body_lo, b.body_hi) for b in out]
 
 
-def oocs_schedule(cfg: Config, steps: int):
+def oocs_schedule(cfg: Config, steps: int, first_sweep: int = 0):
+    """The lowered op list of a run of `steps` steps (oocs_schedule_at: after `first_sweep` sweeps)."""
     n = i64(0)
-    _check(lib().oocs_schedule(ctypes.byref(cfg), steps, None, 0, ctypes.byref(n)), "oocs_schedule")
+    _check(lib().oocs_schedule_at(ctypes.byref(cfg), steps, first_sweep, None, 0, ctypes.byref(n)), "oocs_schedule")
     arr = (Op * n.value)()
-    _check(lib().oocs_schedule(ctypes.byref(cfg), steps, arr, n.value, ctypes.byref(n)), "oocs_schedule")
+    _check(lib().oocs_schedule_at(ctypes.byref(cfg), steps, first_sweep, arr, n.value, ctypes.byref(n)),
+           "oocs_schedule")
     return [dict(kind=OP_KINDS[o.kind], lane=o.lane, g=o.g, block=o.block, sweep=o.sweep, arg=o.arg,
                  ev=(EV_KINDS[o.arg] if o.kind in (6, 7) else None), ev_g=o.ev_g) for o in arr]
 
@@ -282,6 +287,19 @@ def oocs_run(h, steps: int) -> Stats:
     st = Stats()
     _check(lib().oocs_run(h, steps, ctypes.byref(st)), "oocs_run")
     return st
+
+
+def oocs_run_async(h, steps: int):
+    _check(lib().oocs_run_async(h, steps), "oocs_run_async")
+
+
+def oocs_wait(h) -> list:
+    """Complete every run in flight; their Stats in issue order."""
+    n = i64(0)
+    cap = 64
+    arr = (Stats * cap)()
+    _check(lib().oocs_wait(h, arr, cap, ctypes.byref(n)), "oocs_wait")
+    return [arr[i] for i in range(min(n.value, cap))]
 
 
 def oocs_timeline(h):
@@ -370,6 +388,12 @@ class Plan:
 
     def run(self, steps) -> Stats:
         return oocs_run(self.handle, steps)
+
+    def run_async(self, steps):
+        oocs_run_async(self.handle, steps)
+
+    def wait(self) -> list:
+        return oocs_wait(self.handle)
 
     def timeline(self):
         return oocs_timeline(self.handle)

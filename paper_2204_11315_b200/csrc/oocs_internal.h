@@ -40,7 +40,11 @@ struct Geometry {
 };
 
 oocs_status make_geometry(const oocs_config *cfg, Geometry *geo, std::string *err);
-void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops);
+// g0 = global chunk counter of the run's first chunk (runs continue each other's numbering when chainable)
+void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops, int64_t g0 = 0);
+// runs of this plan may be issued back to back without draining in between (oocs_run_async): host store,
+// codec modes, Algorithm 1, one rank
+bool chainable(const Geometry &geo);
 
 // kernels.cu
 // n_arr (<= N_ARRAYS) arrays of the same geometry; BlockQuant does them in one launch

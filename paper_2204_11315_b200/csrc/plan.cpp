@@ -179,7 +179,11 @@ static int send_mask(const Geometry &geo, int blk) {
     return m;
 }
 
-static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
+// g0: global chunk counter of the run's first chunk (a multiple of the rank's chunk count): lanes,
+// working sets and event instances continue across runs, and the first sweep's cross-sweep waits name
+// the previous run's write-backs, so a run can be issued while the previous one drains (oocs_run_async).
+// The ops' `sweep` field stays run-local.  Host store, codec modes only (0 elsewhere).
+static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops, int64_t g0) {
     ops.clear();
     Emitter E{ops};
     const int nb = geo.nb();
@@ -197,14 +201,16 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
     const int L = geo.lanes;
     auto lane = [L](int64_t g) { return (int)(g % L); };
     auto blk_of = [&](int64_t g) { return geo.b_lo + (int)(g % nb); };
-    // previous sweep's chunks whose owned planes intersect [lo, hi)
+    // previous sweep's chunks whose owned planes intersect [lo, hi) (global sweep index; the op keeps
+    // its run-local sweep)
     auto raw_waits = [&](int64_t g, int64_t lo, int64_t hi) {
-        const int t = (int)(g / nb);
-        if (t == 0) return;
+        const int64_t tg = g / nb;
+        if (tg == 0) return;
+        const int t = (int)((g - g0) / nb);
         for (int j = 0; j < nb; ++j) {
             const oocs_block &b = geo.blocks[geo.b_lo + j];
             if (b.own_lo < hi && lo < b.own_hi)
-                E.emit(OOCS_OP_WAIT, lane(g), g, blk_of(g), t, OOCS_EV_D2H, (int64_t)(t - 1) * nb + j);
+                E.emit(OOCS_OP_WAIT, lane(g), g, blk_of(g), t, OOCS_EV_D2H, (tg - 1) * nb + j);
         }
     };
     if (geo.cfg.mode == OOCS_MODE_BASELINE) {
@@ -233,7 +239,7 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
     // ENCODE(p) overwrites (one half-size buffer per stream for both directions): the carry is
     // issued on this same stream before the tail, so stream order protects it.
     auto tail = [&](int64_t p) {
-        const int s = lane(p), blk = blk_of(p), t = (int)(p / nb);
+        const int s = lane(p), blk = blk_of(p), t = (int)((p - g0) / nb);
         E.emit(OOCS_OP_ENCODE, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_ENC, p);
         // multi-GPU: the edge planes go to the neighbour's ghost slot straight from the encoded buffer,
@@ -242,8 +248,8 @@ static void lower_alg1(const Geometry &geo, int64_t sweeps, std::vector<oocs_op>
         E.emit(OOCS_OP_D2H, s, p, blk, t);
         E.emit(OOCS_OP_RECORD, s, p, blk, t, OOCS_EV_D2H, p);
     };
-    for (int64_t g = 0; g < G; ++g) {
-        const int t = (int)(g / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
+    for (int64_t g = g0; g < g0 + G; ++g) {
+        const int t = (int)((g - g0) / nb), i = (int)(g % nb), blk = blk_of(g), s = lane(g);
         const oocs_block &b = geo.blocks[blk];
         const bool carry = i > 0 && b.carry_hi > b.carry_lo;
         // H2D(g) depends only on its stream's own earlier work (the D2H that emptied hf_buf[s], L chunks
@@ -400,7 +406,7 @@ static bool conflict(const std::vector<Acc> &x, const std::vector<Acc> &y) {
 static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std::vector<oocs_op> &ops) {
     // 1. nodes = the sequential program (Algorithm 1's operation order, no synchronisation)
     std::vector<oocs_op> seq;
-    lower_alg1(geo, sweeps, seq);
+    lower_alg1(geo, sweeps, seq, 0);
     std::vector<oocs_op> nodes;
     for (const oocs_op &o : seq)
         if (o.kind != OOCS_OP_WAIT && o.kind != OOCS_OP_RECORD) nodes.push_back(o);
@@ -484,11 +490,16 @@ static void lower_dag(const Geometry &geo, int64_t sweeps, bool by_function, std
     }
 }
 
-void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops) {
+void lower_schedule(const Geometry &geo, int64_t sweeps, std::vector<oocs_op> &ops, int64_t g0) {
     if (geo.host_store && geo.cfg.schedule != OOCS_SCHED_ALG1)
         lower_dag(geo, sweeps, geo.cfg.schedule == OOCS_SCHED_DAG_FUNC, ops);
     else
-        lower_alg1(geo, sweeps, ops);
+        lower_alg1(geo, sweeps, ops, chainable(geo) ? g0 : 0);
+}
+
+bool chainable(const Geometry &geo) {
+    return geo.host_store && geo.cfg.mode != OOCS_MODE_BASELINE && geo.cfg.schedule == OOCS_SCHED_ALG1 &&
+           geo.cfg.world == 1;
 }
 
 }  // namespace oocs
@@ -509,6 +520,11 @@ extern "C" oocs_status oocs_plan_table(const oocs_config *cfg, oocs_block *out) 
 
 extern "C" oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs_op *ops, int64_t cap,
                                      int64_t *n_ops) {
+    return oocs_schedule_at(cfg, steps, 0, ops, cap, n_ops);
+}
+
+extern "C" oocs_status oocs_schedule_at(const oocs_config *cfg, int64_t steps, int64_t first_sweep, oocs_op *ops,
+                                        int64_t cap, int64_t *n_ops) {
     Geometry g;
     std::string err;
     oocs_status st = make_geometry(cfg, &g, &err);
@@ -520,8 +536,12 @@ extern "C" oocs_status oocs_schedule(const oocs_config *cfg, int64_t steps, oocs
         set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
         return OOCS_ERR_CONFIG;
     }
+    if (first_sweep < 0) {
+        set_error("first_sweep must be >= 0");
+        return OOCS_ERR_CONFIG;
+    }
     std::vector<oocs_op> v;
-    lower_schedule(g, steps / g.k, v);
+    lower_schedule(g, steps / g.k, v, first_sweep * g.nb());
     if (n_ops) *n_ops = (int64_t)v.size();
     if (ops && cap > 0) std::memcpy(ops, v.data(), std::min<int64_t>(cap, (int64_t)v.size()) * sizeof(oocs_op));
     return OOCS_OK;

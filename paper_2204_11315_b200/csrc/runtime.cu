@@ -12,6 +12,7 @@
 #include <new>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include <unistd.h>
@@ -77,14 +78,29 @@ struct Plan {
     bool split = false;
     cudaStream_t cstream[3] = {};           // dispatcher: H2D, D2H and D2D (carry) copy streams
     cudaEvent_t cdone[3] = {};
-    std::vector<cudaEvent_t> op_done;       // dispatcher: completion event of every op of a run
+    std::vector<cudaEvent_t> op_done[2];    // dispatcher: completion event of every op of a run, per run slot
     uint64_t copy_chunk = 0;  // pipeline PCIe copies are issued in pieces of this many bytes (0: whole)
     std::vector<cudaEvent_t> ev[6];  // per oocs_event_kind, rings indexed by block counter / DAG node
     int ev_ring = 0;
-    cudaEvent_t t0 = nullptr, t1 = nullptr, lane_done[MAX_LANES] = {};
+    cudaEvent_t t0[2] = {}, t1[2] = {}, lane_done[MAX_LANES] = {};
+    cudaStream_t tstream = nullptr;  // run marks: t0, and t1 after joining every stream of the run
     bool poisoned = false;
-    std::vector<KernelTiming> timing_pool;
-    size_t timing_used = 0;
+    std::vector<KernelTiming> timing_pool[2];
+    size_t timing_used[2] = {0, 0};
+    // Runs issued and not yet finalized, one per slot (oocs_run_async chains at most two in flight: a run
+    // is issued only after the previous one's last op was issued, and the one before that is finalized).
+    // The dispatcher state a chained run needs from its predecessor: every lane's last work op and the op
+    // that produced each event instance (indices into that slot's op_done).
+    struct RunRec {
+        bool active = false;
+        int64_t steps = 0;
+        oocs_stats stats{};
+        std::vector<int64_t> lane_last;
+        std::unordered_map<int64_t, int64_t> producer[6];
+    } runs[2];
+    int slot = 1;              // slot of the most recent run (the first run goes to slot 0)
+    int64_t g_next = 0;        // global chunk counter of the next run's first chunk (chainable plans)
+    std::vector<oocs_stats> finished;  // stats of runs finalized since the last oocs_wait
     // OOCS_FLAG_TIMELINE: one event pair per work op (pool reused across runs) and the last run's spans
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> span_events;
     std::vector<oocs_span> spans;
@@ -239,12 +255,14 @@ static cudaError_t copy_ws_to_raw(void *raw, const float *ws_plane0, const Geome
 // ---------------------------------------------------------------------------
 static KernelTiming *timing_slot(Plan *p, int kind) {
     if (!(p->geo.cfg.flags & OOCS_FLAG_PROFILE)) return nullptr;
-    if (p->timing_used == p->timing_pool.size()) {
+    auto &pool = p->timing_pool[p->slot];
+    size_t &used = p->timing_used[p->slot];
+    if (used == pool.size()) {
         KernelTiming t{kind, nullptr, nullptr};
         if (cudaEventCreate(&t.a) != cudaSuccess || cudaEventCreate(&t.b) != cudaSuccess) return nullptr;
-        p->timing_pool.push_back(t);
+        pool.push_back(t);
     }
-    KernelTiming *t = &p->timing_pool[p->timing_used++];
+    KernelTiming *t = &pool[used++];
     t->kind = kind;
     return t;
 }
@@ -315,7 +333,8 @@ static void free_plan(Plan *p) {
         if (p->cstream[c]) cudaStreamDestroy(p->cstream[c]);
         if (p->cdone[c]) cudaEventDestroy(p->cdone[c]);
     }
-    for (auto e : p->op_done) cudaEventDestroy(e);
+    for (auto &v : p->op_done)
+        for (auto e : v) cudaEventDestroy(e);
     for (int l = 0; l < MAX_LANES; ++l) {
         if (p->split && p->klanes[l] && !p->ext_klane[l]) cudaStreamDestroy(p->klanes[l]);
         if (p->xfer_ev[l]) cudaEventDestroy(p->xfer_ev[l]);
@@ -327,12 +346,15 @@ static void free_plan(Plan *p) {
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : p->lane_done)
         if (e) cudaEventDestroy(e);
-    if (p->t0) cudaEventDestroy(p->t0);
-    if (p->t1) cudaEventDestroy(p->t1);
-    for (auto &t : p->timing_pool) {
-        cudaEventDestroy(t.a);
-        cudaEventDestroy(t.b);
+    for (int k = 0; k < 2; ++k) {
+        if (p->t0[k]) cudaEventDestroy(p->t0[k]);
+        if (p->t1[k]) cudaEventDestroy(p->t1[k]);
+        for (auto &t : p->timing_pool[k]) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
     }
+    if (p->tstream) cudaStreamDestroy(p->tstream);
     for (auto &e : p->span_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -571,7 +593,9 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
                 return OOCS_ERR_CUDA;
             }
     }
-    if (cudaEventCreate(&p->t0) != cudaSuccess || cudaEventCreate(&p->t1) != cudaSuccess) {
+    if (cudaEventCreate(&p->t0[0]) != cudaSuccess || cudaEventCreate(&p->t1[0]) != cudaSuccess ||
+        cudaEventCreate(&p->t0[1]) != cudaSuccess || cudaEventCreate(&p->t1[1]) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->tstream, cudaStreamNonBlocking) != cudaSuccess) {
         set_error("event creation failed");
         free_plan(p);
         return OOCS_ERR_CUDA;
@@ -903,48 +927,64 @@ static bool stalled_ok(Plan *p, std::chrono::steady_clock::time_point since) {
 // the copy-engine scheduler only between DMA commands, and with stream-mapped waits the decode of chunk
 // g was measured to start only once the H2D of chunk g+1 had finished.  Same
 // dependencies as the stream-mapped replay, so the same bytes.
-static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, int cur0, oocs_stats *stats) {
+static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, int cur0, oocs_stats *stats,
+                                    Plan::RunRec *prev) {
     const Geometry &g = p->geo;
     const bool tl = g.cfg.flags & OOCS_FLAG_TIMELINE;
     const size_t n = ops.size();
-    // producer of every event instance (kind, block counter) and the dependency lists
-    std::vector<int64_t> dep_start(n + 1, 0), deps;
+    const int slot = p->slot;
+    Plan::RunRec &me = p->runs[slot];
+    // producer of every event instance (kind, block counter) and the dependency lists; `fdeps` are the
+    // dependencies on ops of the previous run (chained runs, `prev`): that run's ops are all issued, its
+    // events live in the other slot's op_done pool
+    std::vector<int64_t> dep_start(n + 1, 0), deps, fdep_start(n + 1, 0), fdeps;
     {
-        std::vector<int64_t> last_work(g.lanes, -1), pending;
-        std::vector<std::vector<int64_t>> producer(6);
-        auto key = [&](int kind, int64_t eg) -> int64_t & {
-            auto &v = producer[kind];
-            const int64_t i = eg + 1;  // ev_g >= -1
-            if ((int64_t)v.size() <= i) v.resize(i + 1, -1);
-            return v[i];
-        };
-        std::vector<std::vector<int64_t>> lane_waits(g.lanes);
+        std::vector<int64_t> last_work(g.lanes, -1);
+        for (auto &m : me.producer) m.clear();
+        std::vector<std::vector<int64_t>> lane_waits(g.lanes), lane_fwaits(g.lanes);
         for (size_t i = 0; i < n; ++i) {
             const oocs_op &o = ops[i];
             dep_start[i] = (int64_t)deps.size();
+            fdep_start[i] = (int64_t)fdeps.size();
             if (o.kind == OOCS_OP_RECORD) {
-                key(o.arg, o.ev_g) = last_work[o.lane];  // -1: records nothing (trivially complete)
+                if (last_work[o.lane] >= 0) me.producer[o.arg][o.ev_g] = last_work[o.lane];  // else records nothing
             } else if (o.kind == OOCS_OP_WAIT) {
-                const int64_t pr = key(o.arg, o.ev_g);
-                if (pr >= 0) lane_waits[o.lane].push_back(pr);
+                auto it = me.producer[o.arg].find(o.ev_g);
+                if (it != me.producer[o.arg].end()) {
+                    lane_waits[o.lane].push_back(it->second);
+                } else if (prev) {  // an event of the previous run (cross-run RAW, working-buffer hand-off)
+                    auto jt = prev->producer[o.arg].find(o.ev_g);
+                    if (jt != prev->producer[o.arg].end()) lane_fwaits[o.lane].push_back(jt->second);
+                }  // else: never recorded, or recorded by a run that has completed: a no-op
             } else {
                 if (last_work[o.lane] >= 0) deps.push_back(last_work[o.lane]);
+                else if (prev && o.lane < (int)prev->lane_last.size() && prev->lane_last[o.lane] >= 0)
+                    fdeps.push_back(prev->lane_last[o.lane]);  // the lane's program continues across runs
                 for (int64_t d : lane_waits[o.lane]) deps.push_back(d);
+                for (int64_t d : lane_fwaits[o.lane]) fdeps.push_back(d);
                 lane_waits[o.lane].clear();
+                lane_fwaits[o.lane].clear();
                 last_work[o.lane] = (int64_t)i;
             }
         }
         dep_start[n] = (int64_t)deps.size();
+        fdep_start[n] = (int64_t)fdeps.size();
+        // a run of a plan with no chained successor keeps lanes that never worked pointing at the
+        // predecessor's last op on them (chains skip none, but keep the state total)
+        me.lane_last.assign(g.lanes, -1);
+        for (int l = 0; l < g.lanes; ++l) me.lane_last[l] = last_work[l];
     }
-    if (p->op_done.size() < n) {
-        const size_t old = p->op_done.size();
-        p->op_done.resize(n, nullptr);
+    std::vector<cudaEvent_t> &done_ev = p->op_done[slot];
+    if (done_ev.size() < n) {
+        const size_t old = done_ev.size();
+        done_ev.resize(n, nullptr);
         for (size_t i = old; i < n; ++i)
-            if (cudaEventCreateWithFlags(&p->op_done[i], cudaEventDisableTiming) != cudaSuccess) {
-                p->op_done.resize(i);
+            if (cudaEventCreateWithFlags(&done_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+                done_ev.resize(i);
                 CU(cudaErrorMemoryAllocation);
             }
     }
+    const std::vector<cudaEvent_t> *prev_ev = prev ? &p->op_done[slot ^ 1] : nullptr;
     auto stream_of = [&](const oocs_op &o) -> cudaStream_t {
         switch (o.kind) {
         case OOCS_OP_H2D: return p->cstream[0];
@@ -954,22 +994,29 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
     };
     std::vector<char> issued(n, 0), done(n, 0);
     std::vector<cudaStream_t> where(n, nullptr);
+    std::unordered_map<int64_t, char> fdone;  // completion of the previous run's ops polled so far
     for (size_t i = 0; i < n; ++i)
         if (!is_work_op(ops[i].kind)) issued[i] = done[i] = 1;
     // a query error other than NotReady is a sticky device fault: stop and poison the plan
     cudaError_t qerr = cudaSuccess;
-    auto complete = [&](int64_t d) -> bool {
-        if (done[d]) return true;
-        const cudaError_t e = cudaEventQuery(p->op_done[d]);
-        if (e == cudaSuccess) {
-            done[d] = 1;
-            return true;
-        }
-        if (e != cudaErrorNotReady) {
-            qerr = e;
+    auto query = [&](cudaEvent_t e) -> bool {
+        const cudaError_t r = cudaEventQuery(e);
+        if (r == cudaSuccess) return true;
+        if (r != cudaErrorNotReady) {
+            qerr = r;
             (void)cudaGetLastError();
         }
         return false;
+    };
+    auto complete = [&](int64_t d) -> bool {
+        if (done[d]) return true;
+        if (query(done_ev[d])) done[d] = 1;
+        return done[d];
+    };
+    auto fcomplete = [&](int64_t d) -> bool {
+        char &f = fdone[d];
+        if (!f && query((*prev_ev)[d])) f = 1;
+        return f;
     };
     size_t first = 0;
     auto last_progress = std::chrono::steady_clock::now();
@@ -989,13 +1036,18 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
                 const int64_t d = deps[k];
                 ready = issued[d] && (!copy || complete(d));
             }
+            if (copy)
+                for (int64_t k = fdep_start[i]; k < fdep_start[i + 1] && ready; ++k) ready = fcomplete(fdeps[k]);
             if (!ready) continue;
             cudaStream_t st = stream_of(o);
-            if (!copy)
+            if (!copy) {
                 for (int64_t k = dep_start[i]; k < dep_start[i + 1]; ++k) {
                     const int64_t d = deps[k];
-                    if (where[d] != st && !done[d]) CU(cudaStreamWaitEvent(st, p->op_done[d], 0));
+                    if (where[d] != st && !done[d]) CU(cudaStreamWaitEvent(st, done_ev[d], 0));
                 }
+                for (int64_t k = fdep_start[i]; k < fdep_start[i + 1]; ++k)
+                    if (!fdone[fdeps[k]]) CU(cudaStreamWaitEvent(st, (*prev_ev)[fdeps[k]], 0));
+            }
             size_t sp = 0;
             if (tl) {
                 oocs_status r = span_begin(p, o, st, &sp);
@@ -1004,7 +1056,7 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
             oocs_status r = issue_work(p, o, st, cur0, stats);
             if (r) return r;
             if (tl) CU(cudaEventRecord(p->span_events[sp].second, st));
-            CU(cudaEventRecord(p->op_done[i], st));
+            CU(cudaEventRecord(done_ev[i], st));
             issued[i] = 1;
             where[i] = st;
             progress = true;
@@ -1016,94 +1068,62 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
     return OOCS_OK;
 }
 
-static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats *stats) {
+static oocs_status execute(Plan *p, const std::vector<oocs_op> &ops, oocs_stats *stats, Plan::RunRec *prev) {
     const Geometry &g = p->geo;
     const int cur0 = p->cur;
     int64_t sweeps = 0;
     for (const oocs_op &o : ops) sweeps = std::max<int64_t>(sweeps, o.sweep + 1);
     oocs_status r = (g.cfg.flags & (OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS))
                         ? execute_streams(p, ops, cur0, stats)
-                        : execute_dispatch(p, ops, cur0, stats);
+                        : execute_dispatch(p, ops, cur0, stats, prev);
     if (r) return r;
     p->cur = g.host_store ? cur0 : cur0 ^ (int)(sweeps & 1);
     return OOCS_OK;
 }
 
-static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
+// Complete the run in slot k (if it is still in flight): wait for its t1 mark, then its device time,
+// kernel timings, spans and busy fractions; the stats go to p->finished.
+static oocs_status finalize(Plan *p, int k) {
+    Plan::RunRec &r = p->runs[k];
+    if (!r.active) return OOCS_OK;
+    r.active = false;
     const Geometry &g = p->geo;
-    if (steps < 0 || steps % g.k) {
-        set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
-        return OOCS_ERR_CONFIG;
-    }
-    if (g.cfg.world > 1 && !p->connected) {
-        set_error("world > 1: connect the neighbours first (oocs_peer_handle / oocs_peer_connect)");
-        return OOCS_ERR_EXCHANGE;
-    }
-    CU(cudaSetDevice(g.cfg.device));
-    oocs_stats stats;
-    std::memset(&stats, 0, sizeof(stats));
-    std::vector<oocs_op> ops;
-    lower_schedule(g, steps / g.k, ops);
-    p->timing_used = 0;
-    p->spans.clear();
-    p->host_t0 = std::chrono::steady_clock::now();
-    CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->lanes[0]));
-    CU(cudaEventRecord(p->t0, p->lanes[0]));
-    for (int l = 1; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0, 0));
-    if (p->split)
-        for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->klanes[l], p->t0, 0));
-    for (int c = 0; c < 3; ++c) CU(cudaStreamWaitEvent(p->cstream[c], p->t0, 0));
-    oocs_status st = execute(p, ops, &stats);
-    if (st) return poison(p, st);
-    for (int l = 1; l < g.lanes; ++l) {
-        CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
-        CU(cudaStreamWaitEvent(p->lanes[0], p->lane_done[l], 0));
-    }
-    if (p->split)
-        for (int l = 0; l < g.lanes; ++l) {
-            CU(cudaEventRecord(p->kdone[l], p->klanes[l]));
-            CU(cudaStreamWaitEvent(p->lanes[0], p->kdone[l], 0));
-        }
-    for (int c = 0; c < 3; ++c) {
-        CU(cudaEventRecord(p->cdone[c], p->cstream[c]));
-        CU(cudaStreamWaitEvent(p->lanes[0], p->cdone[c], 0));
-    }
-    CU(cudaEventRecord(p->t1, p->lanes[0]));
     {
         // poll instead of blocking: a multi-GPU neighbour that never writes its flag must not hang the
         // process (the watchdog turns it into OOCS_ERR_EXCHANGE and a poisoned plan)
         const auto t_start = std::chrono::steady_clock::now();
         for (;;) {
-            const cudaError_t e = cudaEventQuery(p->t1);
+            const cudaError_t e = cudaEventQuery(p->t1[k]);
             if (e == cudaSuccess) break;
             if (e != cudaErrorNotReady) CU(e);
             if (!stalled_ok(p, t_start)) return poison(p, OOCS_ERR_EXCHANGE);
-            std::this_thread::sleep_for(std::chrono::microseconds(g.cfg.world > 1 ? 20 : 200));
+            std::this_thread::sleep_for(std::chrono::microseconds(g.cfg.world > 1 ? 20 : 100));
         }
     }
+    oocs_stats &stats = r.stats;
     float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, p->t0, p->t1));
+    CU(cudaEventElapsedTime(&ms, p->t0[k], p->t1[k]));
     stats.wall_ms = ms;
-    for (size_t i = 0; i < p->timing_used; ++i) {
+    for (size_t i = 0; i < p->timing_used[k]; ++i) {
         float t = 0.f;
-        CU(cudaEventElapsedTime(&t, p->timing_pool[i].a, p->timing_pool[i].b));
-        stats.kernel_ms[p->timing_pool[i].kind] += t;
+        CU(cudaEventElapsedTime(&t, p->timing_pool[k][i].a, p->timing_pool[k][i].b));
+        stats.kernel_ms[p->timing_pool[k][i].kind] += t;
     }
-    for (size_t i = 0; i < p->spans.size(); ++i) {
-        float a = 0.f, b = 0.f;
-        CU(cudaEventElapsedTime(&a, p->t0, p->span_events[i].first));
-        CU(cudaEventElapsedTime(&b, p->t0, p->span_events[i].second));
-        p->spans[i].start_ms = a;
-        p->spans[i].end_ms = b;
-    }
-    {
+    if (g.cfg.flags & OOCS_FLAG_TIMELINE) {  // timeline runs are never chained: p->spans are this run's
+        for (size_t i = 0; i < p->spans.size(); ++i) {
+            float a = 0.f, b = 0.f;
+            CU(cudaEventElapsedTime(&a, p->t0[k], p->span_events[i].first));
+            CU(cudaEventElapsedTime(&b, p->t0[k], p->span_events[i].second));
+            p->spans[i].start_ms = a;
+            p->spans[i].end_ms = b;
+        }
         // busy time per engine = length of the union of its spans
         std::vector<std::pair<double, double>> iv[4];
-        for (const oocs_span &s : p->spans) {
-            const int e = s.kind == OOCS_OP_H2D ? 0 : s.kind == OOCS_OP_D2H ? 1
-                        : (s.kind == OOCS_OP_DECODE || s.kind == OOCS_OP_STEP || s.kind == OOCS_OP_ENCODE) ? 2
-                        : s.kind == OOCS_OP_SEND ? 3 : -1;
-            if (e >= 0) iv[e].emplace_back(s.start_ms, s.end_ms);
+        for (const oocs_span &sp : p->spans) {
+            const int e = sp.kind == OOCS_OP_H2D ? 0 : sp.kind == OOCS_OP_D2H ? 1
+                        : (sp.kind == OOCS_OP_DECODE || sp.kind == OOCS_OP_STEP || sp.kind == OOCS_OP_ENCODE) ? 2
+                        : sp.kind == OOCS_OP_SEND ? 3 : -1;
+            if (e >= 0) iv[e].emplace_back(sp.start_ms, sp.end_ms);
         }
         for (int e = 0; e < 4; ++e) {
             std::sort(iv[e].begin(), iv[e].end());
@@ -1121,19 +1141,103 @@ static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
             stats.busy_ms[e] = tot;
         }
     }
-    p->seq += steps / g.k;  // the store now holds S_{seq}
     int herr = 0;
     CU(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     stats.data_error = herr;
     int64_t owned = 0;
     for (int i = g.b_lo; i < g.b_hi; ++i) owned += g.blocks[i].own_hi - g.blocks[i].own_lo;
-    stats.cell_updates = (uint64_t)g.nx * g.ny * owned * steps;
-    if (out) *out = stats;
+    stats.cell_updates = (uint64_t)g.nx * g.ny * owned * r.steps;
+    p->finished.push_back(stats);
     if (herr) {
         set_error("encoder rejected a non-finite or |x| >= 2^126 value (S:L200)");
         return OOCS_ERR_DATA;
     }
     return OOCS_OK;
+}
+
+// every run in flight, oldest first
+static oocs_status finalize_all(Plan *p) {
+    oocs_status st = finalize(p, p->slot ^ 1);
+    const oocs_status st2 = finalize(p, p->slot);
+    return st ? st : st2;
+}
+
+// Issue a run.  chain: the caller allows it to start while the previous run drains (oocs_run_async);
+// it does so only for chainable plans (host store, codec modes, Algorithm 1, one rank) on the host
+// dispatcher without a timeline.  Otherwise the previous run is finalized first.  Returns once every
+// op of the run is issued; the run's t1 mark completes with its last op.
+static oocs_status submit(Plan *p, int64_t steps, bool chain) {
+    const Geometry &g = p->geo;
+    if (steps < 0 || steps % g.k) {
+        set_error("steps must be a non-negative multiple of tb_depth (S:L448)");
+        return OOCS_ERR_CONFIG;
+    }
+    if (g.cfg.world > 1 && !p->connected) {
+        set_error("world > 1: connect the neighbours first (oocs_peer_handle / oocs_peer_connect)");
+        return OOCS_ERR_EXCHANGE;
+    }
+    CU(cudaSetDevice(g.cfg.device));
+    const bool can = chain && chainable(g) &&
+                     !(g.cfg.flags & (OOCS_FLAG_TIMELINE | OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS));
+    const int prev = p->slot;
+    const bool chained = can && p->runs[prev].active;
+    if (p->runs[prev].active && !chained)
+        if (oocs_status st = finalize(p, prev)) return st;
+    const int slot = prev ^ 1;
+    if (p->runs[slot].active)  // two runs back: long done when chaining (its successor is fully issued)
+        if (oocs_status st = finalize(p, slot)) return st;
+    std::vector<oocs_op> ops;
+    const int64_t sweeps = steps / g.k;
+    lower_schedule(g, sweeps, ops, p->g_next);
+    if (chainable(g)) p->g_next += sweeps * g.nb();
+    p->slot = slot;
+    p->timing_used[slot] = 0;
+    p->spans.clear();
+    p->host_t0 = std::chrono::steady_clock::now();
+    Plan::RunRec &r = p->runs[slot];
+    std::memset(&r.stats, 0, sizeof(r.stats));
+    r.steps = steps;
+    if (!chained) {
+        // nothing in flight: clear the error flag, and anchor every stream at the run's start mark
+        CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->tstream));
+        CU(cudaEventRecord(p->t0[slot], p->tstream));
+        for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0[slot], 0));
+        if (p->split)
+            for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->klanes[l], p->t0[slot], 0));
+        for (int c = 0; c < 3; ++c) CU(cudaStreamWaitEvent(p->cstream[c], p->t0[slot], 0));
+    } else {
+        // the mark follows the previous run's t1 on the timing stream: the time this run's first ops
+        // overlap with the previous run's drain is counted once, in the previous run
+        CU(cudaEventRecord(p->t0[slot], p->tstream));
+    }
+    oocs_status st = execute(p, ops, &r.stats, chained ? &p->runs[prev] : nullptr);
+    if (st) return poison(p, st);
+    // t1: after every stream's share of this run
+    for (int l = 0; l < g.lanes; ++l) {
+        CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
+        CU(cudaStreamWaitEvent(p->tstream, p->lane_done[l], 0));
+        if (p->split) {
+            CU(cudaEventRecord(p->kdone[l], p->klanes[l]));
+            CU(cudaStreamWaitEvent(p->tstream, p->kdone[l], 0));
+        }
+    }
+    for (int c = 0; c < 3; ++c) {
+        CU(cudaEventRecord(p->cdone[c], p->cstream[c]));
+        CU(cudaStreamWaitEvent(p->tstream, p->cdone[c], 0));
+    }
+    CU(cudaEventRecord(p->t1[slot], p->tstream));
+    r.active = true;
+    p->seq += sweeps;  // the store holds S_{seq} once this run completes
+    return OOCS_OK;
+}
+
+static oocs_status run(Plan *p, int64_t steps, oocs_stats *out) {
+    if (oocs_status st = submit(p, steps, false)) return st;
+    p->finished.clear();
+    oocs_status st = finalize(p, p->slot);
+    if (out && !p->finished.empty()) *out = p->finished.back();
+    p->finished.clear();
+    return st;
 }
 
 // ---------------------------------------------------------------------------
@@ -1497,37 +1601,44 @@ oocs_status oocs_peer_connect(oocs_plan *plan, const void *lower, const void *up
 }
 
 oocs_status oocs_destroy(oocs_plan *plan) {
+    if (plan && !plan->poisoned) (void)finalize_all(plan);  // let runs in flight finish before freeing
     free_plan(static_cast<Plan *>(plan));
     return OOCS_OK;
 }
 
 oocs_status oocs_load(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, load(plan, array, src, a_lo, a_hi, false));
 }
 
 oocs_status oocs_load_device(oocs_plan *plan, int32_t array, const float *src, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, load(plan, array, src, a_lo, a_hi, true));
 }
 
 oocs_status oocs_store(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, store(plan, array, dst, a_lo, a_hi, false));
 }
 
 oocs_status oocs_store_device(oocs_plan *plan, int32_t array, float *dst, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, store(plan, array, dst, a_lo, a_hi, true));
 }
 
 oocs_status oocs_store_read_raw(oocs_plan *plan, int32_t array, void *dst, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, raw_io(plan, array, dst, a_lo, a_hi, false));
 }
 
 oocs_status oocs_store_write_raw(oocs_plan *plan, int32_t array, const void *src, int64_t a_lo, int64_t a_hi) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = poison(plan, finalize_all(plan))) return st;  // runs in flight complete first
     return poison(plan, raw_io(plan, array, const_cast<void *>(src), a_lo, a_hi, true));
 }
 
@@ -1536,8 +1647,28 @@ oocs_status oocs_run(oocs_plan *plan, int64_t steps, oocs_stats *out) {
     return poison(plan, run(plan, steps, out));
 }
 
+oocs_status oocs_run_async(oocs_plan *plan, int64_t steps) {
+    if (oocs_status st = guard(plan)) return st;
+    return poison(plan, submit(plan, steps, true));
+}
+
+oocs_status oocs_wait(oocs_plan *plan, oocs_stats *out, int64_t cap, int64_t *n_runs) {
+    if (oocs_status st = guard(plan)) return st;
+    if (cap < 0 || (cap > 0 && !out)) {
+        set_error("oocs_wait: out is NULL or cap < 0");
+        return OOCS_ERR_CONFIG;
+    }
+    const oocs_status st = poison(plan, finalize_all(plan));
+    const int64_t n = (int64_t)plan->finished.size();
+    if (n_runs) *n_runs = n;
+    for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = plan->finished[i];
+    plan->finished.clear();
+    return st;
+}
+
 oocs_status oocs_timeline(const oocs_plan *plan, oocs_span *out, int64_t cap, int64_t *n_spans) {
     if (oocs_status st = guard(plan)) return st;
+    if (oocs_status st = finalize_all(const_cast<oocs_plan *>(plan))) return st;
     if (!n_spans || cap < 0) {
         set_error("oocs_timeline: n_spans is NULL or cap < 0");
         return OOCS_ERR_CONFIG;

@@ -374,3 +374,37 @@ def test_schedule_race_free_random_configs():
                 continue
             assert sum(o["kind"] == kind for o in ops) == sweeps * n * per
         done += 1
+
+
+@pytest.mark.parametrize("mode", ["swb", "dwb", "compress"])
+@pytest.mark.parametrize("n,k,nz,lanes", [(4, 2, 64, 0), (16, 1, 128, 2), (2, 1, 32, 0), (5, 3, 80, 2), (1, 1, 16, 0)])
+def test_chained_runs_are_race_free(mode, n, k, nz, lanes):
+    """oocs_run_async issues a run while the previous one drains: the dispatcher sees the two op lists
+    back to back (lane programs and events continue across them).  Their concatenation must be race-free
+    under stream + event semantics, and the second run's first H2Ds must carry the cross-sweep waits on
+    the first run's write-backs -- deleting them is a detected race."""
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, n_lanes=lanes)
+    s1, s2, s3 = 2 * k, k, 3 * k
+    ops = (oocs.oocs_schedule(c, s1) + oocs.oocs_schedule(c, s2, first_sweep=s1 // k)
+           + oocs.oocs_schedule(c, s3, first_sweep=(s1 + s2) // k))
+    blocks = oocs.oocs_plan_table(c)
+    geo = _geo(c, blocks)
+    assert sc.violations(ops, blocks, geo) == []
+    assert sum(o["kind"] == "STEP" for o in ops) == n * (s1 + s2 + s3)
+    # the chunk counter continues: every global chunk is decoded exactly once
+    dec = [o["g"] for o in ops if o["kind"] == "DECODE"]
+    assert dec == list(range(n * (s1 + s2 + s3) // k))
+    n1 = len(oocs.oocs_schedule(c, s1))
+    cross = [i for i, o in enumerate(ops) if i >= n1 and o["kind"] == "WAIT" and o["ev"] == "D2H"
+             and o["ev_g"] < (s1 // k) * n]
+    assert cross, "the second run must wait on the first run's write-backs"
+    caught = sum(bool(sc.violations(ops[:i] + ops[i + 1:], blocks, geo, limit=1)) for i in cross)
+    assert caught >= 1
+
+
+def test_schedule_at_is_a_restart_where_runs_cannot_chain():
+    # DAG schedules, the BASELINE mode, the device store and multi-rank plans restart at chunk 0
+    for kw in (dict(schedule="dag"), dict(mode="baseline", codec="identity", rate_bits=32), dict(store="device"),
+               dict(world=2, rank=0)):
+        c = cfg(nz=64, n_blocks=4, tb_depth=2, **kw)
+        assert oocs.oocs_schedule(c, 4, first_sweep=3) == oocs.oocs_schedule(c, 4)
