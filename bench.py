@@ -80,6 +80,8 @@ def parse():
     # c3 33.01 vs 33.01) with one half-size staging buffer less, -20% device memory
     ap.add_argument("--lanes", type=int, default=2, help="pipeline lanes of the compressed modes (Alg. 1's strm[0:3] "
                     "= 3; each lane owns one half-size staging buffer)")
+    ap.add_argument("--sync-steps", action="store_true", help="blocking oocs_run per step instead of "
+                    "oocs_run_async (no overlap of one step's drain with the next step's fill)")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
                     help="stream/event schedule of the host-store pipeline (e2e)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -525,9 +527,12 @@ def main():
     barrier()
     t0 = time.perf_counter()
     with clocks:
-        for _ in range(args.steps):
-            host.run_async(T)
-        per = host.wait()
+        if args.sync_steps:
+            per = [host.run(T) for _ in range(args.steps)]
+        else:
+            for _ in range(args.steps):
+                host.run_async(T)
+            per = host.wait()
         barrier()
         # the host clock stops here: stopping the nvidia-smi sampler (it finishes its current query
         # first, up to ~1 s) is not part of the K steps
