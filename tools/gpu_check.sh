@@ -1,5 +1,4 @@
-# end-of-round check on the final code: the -m gpu suite, compute-sanitizer, the ncu launch list of the
-# bench command, and the bench line
+# end-of-round check on the final code: the -m gpu suite, compute-sanitizer, and the bench line
 export OOCS_REPORT_DIR=gpurun_out/rep
 timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -4
 mkdir -p gpurun_out/sanitizer
@@ -7,6 +6,4 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > gpurun_out/sanitizer/sanitize_$tool.log 2>&1
   echo "== $tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY" gpurun_out/sanitizer/sanitize_$tool.log | head -3
 done
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1; tail -c 200 gpurun_out/bench_under_ncu.log
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -c 300 gpurun_out/bench_final.json
