@@ -32,3 +32,15 @@ for codec, rate in (("blockquant", 16), ("blockquant", 24), ("zfp", 12), ("trunc
         assert np.isfinite(out).all()
         pl.close()
         print("ok", codec, rate, store, sched, mode, extra, flush=True)
+# chained runs (oocs_run_async): a run issued while the previous one drains
+c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=3, tb_depth=2, codec="blockquant",
+                     rate_bits=16, mode="swb", store="host", n_lanes=2)
+pl = oocs.Plan(c)
+for a, arr in enumerate((vel, p0, p0)):
+    pl.load(a, arr, 0, az)
+for _ in range(3):
+    pl.run_async(2)
+assert len(pl.wait()) == 3
+assert np.isfinite(pl.store(2, 0, az)).all()
+pl.close()
+print("ok chained", flush=True)
