@@ -187,7 +187,8 @@ typedef struct {
 } oocs_plan_info;
 
 typedef struct {
-    double wall_ms;             /* device time of the run: event on first op .. event after last op */
+    double wall_ms;             /* device time of the run: its start mark .. the mark after its last op; a chained
+                                 * run's start mark follows the previous run's end mark (oocs_run_async) */
     double kernel_ms[3];        /* [decode, step, encode] summed launch durations (OOCS_FLAG_PROFILE) */
     int64_t kernel_launches[3]; /* launches per kind */
     uint64_t bytes_h2d, bytes_d2h, bytes_d2d, bytes_exchange;
