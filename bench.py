@@ -84,6 +84,8 @@ def parse():
                     "oocs_run_async (no overlap of one step's drain with the next step's fill)")
     ap.add_argument("--schedule", default="alg1", choices=["alg1", "dag", "dag_func"],
                     help="stream/event schedule of the host-store pipeline (e2e)")
+    ap.add_argument("--fuse-decode", action="store_true", help="OOCS_FLAG_FUSE_DECODE: the first step of each "
+                    "chunk reads p_{t-1} from its compressed records (decode -> first step fusion, NEXT-2)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-rank path with several ranks sharing one GPU")
     return ap.parse_args()
@@ -469,7 +471,8 @@ def main():
                              rate_bits=rate if codec != "identity" else 32, mode=mode, store=store, device=local,
                              rank=rank if wl is None else 0, world=world if wl is None else 1,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
-                             decoded_velocity=decoded_velocity, n_lanes=0 if mode == "baseline" else args.lanes)
+                             decoded_velocity=decoded_velocity, n_lanes=0 if mode == "baseline" else args.lanes,
+                             fuse_decode=args.fuse_decode and mode != "baseline" and codec == "blockquant")
         pl = oocs.Plan(c)
         if world > 1 and wl is None:
             odist.connect(pl, gloo=gloo)

@@ -136,6 +136,14 @@ typedef enum {
  * bitwise identical; each chunk's decode then moves two arrays instead of three.  Decoded once per
  * oocs_load / oocs_store_write_raw of array 0.  Off by default (the compressed-state accounting). */
 #define OOCS_FLAG_DECODED_VELOCITY 64u
+/* Decode -> first step fusion: the first of a chunk's k steps reads p_{t-1} straight
+ * from its compressed BlockQuant records (staged into shared memory by bulk copies, decoded with the decode
+ * kernel's warp transpose and arithmetic) instead of a decoded working-buffer copy, and the chunk's decode
+ * then writes only the velocity, p_t and the x/y ring of p_{t-1} (which later steps read as the boundary).
+ * p_{t-1} is read once and then overwritten, so this saves 8 B per cell of decode write + step read.  Same
+ * values, so results are bitwise identical.  Codec modes with BlockQuant at an even rate <= 16 (q odd,
+ * 16-byte records) and the 25-point stencil; chunks with multi-GPU ghost planes run unfused. */
+#define OOCS_FLAG_FUSE_DECODE 128u
 #define OOCS_FLAG_LANE_SINGLE_STREAM 16u
 #define OOCS_FLAG_LANE_SPLIT_STREAMS 32u
 

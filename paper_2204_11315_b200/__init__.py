@@ -45,6 +45,7 @@ FLAG_TIMELINE = 8
 FLAG_LANE_SINGLE_STREAM = 16
 FLAG_LANE_SPLIT_STREAMS = 32
 FLAG_DECODED_VELOCITY = 64
+FLAG_FUSE_DECODE = 128
 EXECUTOR = {"dispatch": 0, "single": FLAG_LANE_SINGLE_STREAM, "split": FLAG_LANE_SPLIT_STREAMS}
 OP_KINDS = ["H2D", "CARRY", "DECODE", "STEP", "ENCODE", "D2H", "RECORD", "WAIT", "SEND"]
 PEER_HANDLE_BYTES = 256
@@ -164,7 +165,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
                 region_sharing=True, store="host", device=0, rank=0, world=1, profile=False,
                 device_capacity=0, n_lanes=0, resident_velocity=False, schedule="alg1",
                 timeline=False, executor="dispatch", decoded_velocity=False, stencil="acoustic25", v_max=0.0,
-                ext_streams=()) -> Config:
+                ext_streams=(), fuse_decode=False) -> Config:
     """ext_streams: up to 8 integer cudaStream_t handles (e.g. torch.cuda.Stream().cuda_stream), lane order."""
     c = Config()
     c.struct_size = ctypes.sizeof(Config)
@@ -181,7 +182,7 @@ def make_config(nx, ny, nz, dt, n_blocks, tb_depth, codec="blockquant", rate_bit
     c.device, c.rank, c.world = device, rank, world
     c.flags = ((FLAG_PROFILE if profile else 0) | (FLAG_RESIDENT_VELOCITY if resident_velocity else 0)
                | (FLAG_TIMELINE if timeline else 0) | EXECUTOR[executor]
-               | (FLAG_DECODED_VELOCITY if decoded_velocity else 0))
+               | (FLAG_DECODED_VELOCITY if decoded_velocity else 0) | (FLAG_FUSE_DECODE if fuse_decode else 0))
     c.device_capacity = device_capacity
     c.stencil = STENCIL[stencil] if isinstance(stencil, str) else stencil
     c.v_max = float(v_max)

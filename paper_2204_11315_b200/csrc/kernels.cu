@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "oocs_internal.h"
@@ -109,10 +110,24 @@ __device__ __forceinline__ uint32_t pat_hi(uint32_t w) { return __byte_perm(w, 0
 struct LineTask {
     int bz, by, b0, nb;
 };
-__device__ __forceinline__ LineTask line_task(int nbx, int bz) {
+// ring_nl > 0 (decode only): a compact grid over the x/y ring of the allocated grid -- x in [0, 2 nl):
+// the first / last group of 8 block rows of every line, x in [2 nl, 2 nl + 2 ng): the first / last line of
+// every group (corners twice, same values)
+__device__ __forceinline__ LineTask line_task(int nbx, int bz, int ring_nl = 0, int ring_ng = 0) {
     LineTask t;
-    const int L = blockIdx.x;
-    t.by = blockIdx.y * 8 + (threadIdx.x >> 5);
+    int L = blockIdx.x, grp = blockIdx.y;
+    if (ring_nl) {
+        int i = blockIdx.x;
+        if (i < 2 * ring_nl) {
+            grp = i < ring_nl ? 0 : ring_ng - 1;
+            L = i < ring_nl ? i : i - ring_nl;
+        } else {
+            i -= 2 * ring_nl;
+            L = i < ring_ng ? 0 : ring_nl - 1;
+            grp = i < ring_ng ? i : i - ring_ng;
+        }
+    }
+    t.by = grp * 8 + (threadIdx.x >> 5);
     t.bz = bz;
     t.b0 = L == 0 ? 0 : 8 * L - 7;
     const int b1 = min(nbx - 1, 8 * L);
@@ -128,6 +143,7 @@ struct CodecArrays {
     const void *src[N_ARRAYS];
     void *dst[N_ARRAYS];
     int slabs;  // 4-plane slabs per array
+    int ring_nl, ring_ng;  // decode: > 0 = the x/y ring only (line_task)
     // selects, not a dynamic index: an indexed kernel-parameter array would be copied to local memory
     __device__ __forceinline__ const void *in(int a) const { return a == 0 ? src[0] : a == 1 ? src[1] : src[2]; }
     __device__ __forceinline__ void *out(int a) const { return a == 0 ? dst[0] : a == 1 ? dst[1] : dst[2]; }
@@ -148,7 +164,7 @@ bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
     const int arr = blockIdx.z / A.slabs;
     const uint8_t *__restrict__ src = static_cast<const uint8_t *>(A.in(arr));
     float *__restrict__ dst = static_cast<float *>(A.out(arr));
-    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
+    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs, A.ring_nl, A.ring_ng);
     if (t.by >= nby) return;
     const int recw = 2 * (q + 1);  // record size in 32-bit words
     const uint32_t *rec0 = reinterpret_cast<const uint32_t *>(src) +
@@ -500,6 +516,30 @@ struct S2Smem {
 };
 constexpr int S2_TX = 64, S2_NB = 3, S2_D = 2;
 
+// Decode -> first step (NEXT-2, OOCS_FLAG_FUSE_DECODE): the first of a chunk's k steps reads p_{t-1} straight
+// from its compressed BlockQuant records instead of a decoded working-buffer copy -- p_{t-1} is read once,
+// by this step, and then overwritten by p_{t+1}, so decoding it to HBM and reading it back is 8 B per value
+// of pure traffic.  Per 4-plane slab the CTA's 16 x 4 records (one bulk copy per block row, one slab ahead,
+// on their own mbarriers) are decoded by the 8 warps with the decode kernel's warp transpose into a 16-bit
+// code tile, and each thread reconstructs its own cells with the decode kernel's arithmetic (bitwise the
+// same values).  q odd and <= 15: 16-byte records.  NF = number of arrays read this way (1; the velocity
+// as a second one was measured slower -- it must still be written decoded for the later steps, so it
+// saves 4 B per value for the same decode work: DESIGN.md §6).
+constexpr int FS_ROWP = 68;              // u16 per code row (64 + 4): 34 words, rows 2 banks apart
+constexpr int FS_PLANEP = 16 * 68 + 16;  // u16 per code plane: 552 words, planes 8 banks apart -> the
+                                         // transpose's scatter (8 rows x 2 words per block) is conflict-free
+constexpr int FS_RECW = 32;              // max record words (q <= 15)
+template <int TY, int NF>
+struct S2SmemF {
+    float p[S2_NS][TY + 2 * R][64 + 2 * R];
+    float v[3][TY][64];
+    uint32_t stage[NF][2][TY / 4][16 * FS_RECW];  // records of a slab: 16 per block row (double-buffered)
+    uint16_t cs[NF][4 * FS_PLANEP];               // codes of the slab: [plane][row][x]
+    float2 hdr[NF][TY / 4][16];                   // (mn, step) per block
+    unsigned long long bar[4];
+    unsigned long long sbar[2];
+};
+
 // coefficients of d2/dx2, order 8 (Q1): 8/5, -1/5, 8/315, -1/560
 #define C1 1.6f
 #define C2 (-0.2f)
@@ -541,14 +581,88 @@ struct StepArgs {
     int nx, ny, z_lo, z_hi, zchunk, gx;
     int64_t pitch, pstride;
     float dt;
+    // fused decode (S2SmemF): records of the chunk extent's first slab of p_{t-1}, blocks per row / column
+    // of the allocated grid, code bits, record words
+    const uint32_t *rec[1];
+    int nbx, nby, q, recw;
 };
 
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// one thread: bulk-copy slab bz's records of the tile (block rows y0/4+1.., columns x0/4+1..+15) of each
+// fused array into stage buf
+template <int TY, int NF>
+__device__ __forceinline__ void fuse_stage(S2SmemF<TY, NF> &S, const StepArgs &a, int bz, int buf, int x0, int y0) {
+    const int bx0 = x0 / 4 + 1, nblk = min(16, a.nbx - bx0);
+    const uint32_t row_bytes = (uint32_t)(nblk * a.recw * 4);
+    int rows = 0;
+#pragma unroll
+    for (int r = 0; r < TY / 4; ++r) rows += (y0 / 4 + 1 + r < a.nby) ? 1 : 0;
+    mbar_expect_tx(&S.sbar[buf], NF * rows * row_bytes);
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int r = 0; r < TY / 4; ++r) {
+            const int by = y0 / 4 + 1 + r;
+            if (by < a.nby)
+                bulk_load(&S.stage[f][buf][r][0],
+                          a.rec[f] + ((int64_t)bz * a.nby + by) * a.nbx * a.recw + (int64_t)bx0 * a.recw, row_bytes,
+                          &S.sbar[buf]);
+        }
+}
+
+// every warp, per fused array: decode its 8 records (block row warp/2, columns 8 (warp&1) ..) of stage buf
+// into the code tile (same transpose and (mn, step) arithmetic as bq_decode_kernel)
+template <int TY, int NF>
+__device__ __forceinline__ void fuse_decode(S2SmemF<TY, NF> &S, const StepArgs &a, int buf, int x0, int y0, int lane,
+                                            int warp) {
+    const int r = warp >> 1, bl0 = 8 * (warp & 1), q = a.q, recw = a.recw;
+    const int nbv = (y0 / 4 + 1 + r < a.nby) ? min(8, max(0, a.nbx - (x0 / 4 + 1 + bl0))) : 0;
+    const int b = lane & 15, half = lane >> 4;
+    const int w0i = b < q ? 2 + 2 * (q - 1 - b) + half : -1;
+    const Xpose X(lane);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        const uint32_t *st = &S.stage[f][buf][r][bl0 * recw];
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = (i < nbv && w0i >= 0) ? st[i * recw + w0i] : 0u;
+        const uint32_t hdr = (lane < 16 && (lane & 7) < nbv) ? st[(lane & 7) * recw + (lane >> 3)] : 0u;
+        const float mx_l = __uint_as_float(__shfl_down_sync(0xffffffffu, hdr, 8));
+        const float mn_l = __uint_as_float(hdr);
+        if (lane < 8) S.hdr[f][r][bl0 + lane] = make_float2(mn_l, __fmul_rn(__fsub_rn(mx_l, mn_l), pow2f(-q)));
+        // lane m holds codes m (low half) and m + 32 (high half): j = xi + 4 yi + 16 zi
+        uint16_t *c = S.cs[f] + (lane >> 4) * FS_PLANEP + (4 * r + ((lane >> 2) & 3)) * FS_ROWP + 4 * bl0 + (lane & 3);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t y = X(w[i]);
+            c[4 * i] = (uint16_t)y;
+            c[4 * i + 2 * FS_PLANEP] = (uint16_t)(y >> 16);
+        }
+    }
+}
+
+// the two cells (x, x+1) of row y of plane zi of fused array f: x = fma((float)code + 0.5, step, mn), as
+// bq_decode_kernel's put()
+template <typename SM>
+__device__ __forceinline__ float2 fuse_value(const SM &S, int f, int zi, int y, int x, float2 hm) {
+    const uint32_t c = *reinterpret_cast<const uint32_t *>(S.cs[f] + zi * FS_PLANEP + y * FS_ROWP + x);
+    const float2 h = make_float2(-8388607.5f, -8388607.5f);
+    return __ffma2_rn(__fadd2_rn(make_float2(__uint_as_float(pat_lo(c)), __uint_as_float(pat_hi(c))), h),
+                      make_float2(hm.y, hm.y), make_float2(hm.x, hm.x));
+}
+
 // one plane of the march; OFF = (z - zs) mod 9 is a compile-time register-queue rotation
-template <int OFF, int TY>
-__device__ __forceinline__ bool s2_plane(S2Smem<TY> &S, const CUtensorMap *mP, const CUtensorMap *mPP,
+template <int OFF, int TY, int NF, typename SM>
+__device__ __forceinline__ bool s2_plane(SM &S, const CUtensorMap *mP, const CUtensorMap *mPP,
                                          const CUtensorMap *mV, const StepArgs &a, int z, int zs, int ze,
                                          int x0, int y0, float2 (&q)[9][2], uint32_t &ph, bool okr0,
-                                         bool okr1, int64_t g0) {
+                                         bool okr1, int64_t g0, float2 (&hm)[1]) {
     if (z >= ze) return false;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // every thread is done with plane z-1: its ring slots may be refilled
@@ -558,10 +672,21 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY> &S, const CUtensorMap *mP, c
         constexpr int ps = (OFF + 4 + S2_D + R) % NS;  // slot of plane z+D+4 (previously plane z+D+4-NS)
         constexpr int st = (OFF + S2_D) % S2_NB;     // stage of plane z+D
         unsigned long long *bar = &S.bar[st];
-        mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
+        mbar_expect_tx(bar, S2T<TY>::PBYTES + (2 - NF) * S2T<TY>::TBYTES);
         tma_load_3d(&S.p[ps][0][0], mP, XOFF + x0, y0, z + S2_D + R, bar);
-        tma_load_3d(&S.pp[st][0][0], mPP, XOFF + R + x0, R + y0, z + S2_D, bar);
+        if constexpr (NF == 0) tma_load_3d(&S.pp[st][0][0], mPP, XOFF + R + x0, R + y0, z + S2_D, bar);
         tma_load_3d(&S.v[st][0][0], mV, XOFF + R + x0, R + y0, z + S2_D, bar);
+    }
+    if constexpr (NF > 0) {
+        if (((z - zs) & 3) == 0) {  // a new slab: decode it (its records arrived one slab ago)
+            const int j = (z - zs) >> 2;
+            if (tid == 0 && z + 4 < ze) fuse_stage<TY, NF>(S, a, (z >> 2) + 1, (j + 1) & 1, x0, y0);
+            mbar_wait(&S.sbar[j & 1], (uint32_t)(j >> 1) & 1u);
+            fuse_decode<TY, NF>(S, a, j & 1, x0, y0, lane, warp);
+            __syncthreads();
+#pragma unroll
+            for (int f = 0; f < NF; ++f) hm[f] = S.hdr[f][warp >> 1][lane >> 1];
+        }
     }
     constexpr int st = OFF % S2_NB;
     mbar_wait(&S.bar[st], (ph >> st) & 1u);
@@ -579,10 +704,17 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY> &S, const CUtensorMap *mP, c
         if (m != 4 && m != 5) yr[m] = *reinterpret_cast<const float2 *>(&P[cy + m][R + cx]);
     yr[4] = q[(OFF + 4) % 9][0];
     yr[5] = q[(OFF + 4) % 9][1];
-    const float2 pp0 = *reinterpret_cast<const float2 *>(&S.pp[st][cy][cx]);
-    const float2 pp1 = *reinterpret_cast<const float2 *>(&S.pp[st][cy + 1][cx]);
-    const float2 v0 = *reinterpret_cast<const float2 *>(&S.v[st][cy][cx]);
-    const float2 v1 = *reinterpret_cast<const float2 *>(&S.v[st][cy + 1][cx]);
+    float2 pp0, pp1, v0, v1;
+    if constexpr (NF > 0) {
+        const int zi = (z - zs) & 3;
+        pp0 = fuse_value(S, 0, zi, cy, cx, hm[0]);
+        pp1 = fuse_value(S, 0, zi, cy + 1, cx, hm[0]);
+    } else {
+        pp0 = *reinterpret_cast<const float2 *>(&S.pp[st][cy][cx]);
+        pp1 = *reinterpret_cast<const float2 *>(&S.pp[st][cy + 1][cx]);
+    }
+    v0 = *reinterpret_cast<const float2 *>(&S.v[st][cy][cx]);
+    v1 = *reinterpret_cast<const float2 *>(&S.v[st][cy + 1][cx]);
     // The two x-adjacent cells of a row go through Blackwell's paired fp32 pipe (FADD2 / FMUL2 /
     // FFMA2): every operation is the same IEEE-rounded scalar operation as before, on both cells at
     // once, so results are bitwise those of the scalar form below (difference form, x-y-z FMA chain):
@@ -625,12 +757,13 @@ __device__ __forceinline__ bool s2_plane(S2Smem<TY> &S, const CUtensorMap *mP, c
     return true;
 }
 
-template <int TY>
+template <int TY, int NF>
 __global__ void __launch_bounds__(S2T<TY>::THREADS, S2T<TY>::CTAS)
 stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mPP,
                         const __grid_constant__ CUtensorMap mV, const StepArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    S2Smem<TY> &S = *reinterpret_cast<S2Smem<TY> *>(smem_raw);
+    using SM = std::conditional_t<NF == 0, S2Smem<TY>, S2SmemF<TY, NF>>;
+    SM &S = *reinterpret_cast<SM *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int x0 = blockIdx.x * S2_TX, y0 = blockIdx.y * TY;
     const int zs = a.z_lo + blockIdx.z * a.zchunk;
@@ -643,6 +776,10 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
     const int64_t g0 = (int64_t)(y + R) * a.pitch + x + R + XOFF;
     if (tid == 0) {
         for (int i = 0; i <= S2_NB; ++i) mbar_init(&S.bar[i], 1);
+        if constexpr (NF > 0) {
+            mbar_init(&S.sbar[0], 1);
+            mbar_init(&S.sbar[1], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -653,13 +790,14 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
         mbar_expect_tx(pro, 4 * S2T<TY>::PBYTES);
         constexpr int NS = S2_NS;
         for (int i = 0; i < 4; ++i) tma_load_3d(&S.p[(4 + i) % NS][0][0], &mP, XOFF + x0, y0, zs + i, pro);
+        if constexpr (NF > 0) fuse_stage<TY, NF>(S, a, zs >> 2, 0, x0, y0);  // records of the first slab
         for (int j = 0; j < S2_D; ++j) {
             const int z = zs + j;
             if (z >= ze) break;
             unsigned long long *bar = &S.bar[j % S2_NB];
-            mbar_expect_tx(bar, S2T<TY>::PBYTES + 2 * S2T<TY>::TBYTES);
+            mbar_expect_tx(bar, S2T<TY>::PBYTES + (2 - NF) * S2T<TY>::TBYTES);
             tma_load_3d(&S.p[(j + 4 + R) % NS][0][0], &mP, XOFF + x0, y0, z + R, bar);
-            tma_load_3d(&S.pp[j % S2_NB][0][0], &mPP, XOFF + R + x0, R + y0, z, bar);
+            if constexpr (NF == 0) tma_load_3d(&S.pp[j % S2_NB][0][0], &mPP, XOFF + R + x0, R + y0, z, bar);
             tma_load_3d(&S.v[j % S2_NB][0][0], &mV, XOFF + R + x0, R + y0, z, bar);
         }
     }
@@ -677,16 +815,17 @@ stencil_step_tma_kernel(const __grid_constant__ CUtensorMap mP, const __grid_con
     q[8][0] = q[8][1] = make_float2(0.f, 0.f);
     mbar_wait(&S.bar[S2_NB], 0);
     uint32_t ph = 0;
+    float2 hm[1] = {make_float2(0.f, 0.f)};
     for (int zb = zs; zb < ze; zb += 9) {
-        if (!s2_plane<0, TY>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<1, TY>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<2, TY>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<3, TY>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<4, TY>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<5, TY>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<6, TY>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<7, TY>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
-        if (!s2_plane<8, TY>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0)) break;
+        if (!s2_plane<0, TY, NF>(S, &mP, &mPP, &mV, a, zb + 0, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<1, TY, NF>(S, &mP, &mPP, &mV, a, zb + 1, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<2, TY, NF>(S, &mP, &mPP, &mV, a, zb + 2, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<3, TY, NF>(S, &mP, &mPP, &mV, a, zb + 3, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<4, TY, NF>(S, &mP, &mPP, &mV, a, zb + 4, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<5, TY, NF>(S, &mP, &mPP, &mV, a, zb + 5, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<6, TY, NF>(S, &mP, &mPP, &mV, a, zb + 6, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<7, TY, NF>(S, &mP, &mPP, &mV, a, zb + 7, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
+        if (!s2_plane<8, TY, NF>(S, &mP, &mPP, &mV, a, zb + 8, zs, ze, x0, y0, q, ph, okr0, okr1, g0, hm)) break;
     }
 }
 
@@ -1135,6 +1274,33 @@ cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, 
     return cudaGetLastError();
 }
 
+// BlockQuant, one array: decode only the blocks of the x/y ring (bx = 0, nbx-1; by = 0, nby-1) of every slab,
+// with their lines / row groups (the fused first step overwrites the interior)
+cudaError_t launch_decode_ring(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch, int q,
+                               cudaStream_t st) {
+    if (planes <= 0) return cudaSuccess;
+    const int nbx = (int)(ax / 4), nby = (int)(ay / 4);
+    CodecArrays A{};
+    A.src[0] = src;
+    A.dst[0] = dst;
+    A.slabs = (int)(planes / 4);
+    A.ring_nl = (int)nlines_of(ax);
+    A.ring_ng = (nby + 7) / 8;
+    const dim3 blocks((unsigned)(2 * A.ring_nl + 2 * A.ring_ng), 1u, (unsigned)A.slabs);
+    const int64_t pstride = ay * pitch;
+#define DEC(TWO, QT) bq_decode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q)
+    switch (q) {
+    case 7: DEC(false, 7); break;
+    case 11: DEC(false, 11); break;
+    case 15: DEC(false, 15); break;
+    default:
+        if (q > 16) DEC(true, 0);
+        else DEC(false, 0);
+    }
+#undef DEC
+    return cudaGetLastError();
+}
+
 cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, int64_t ax, int64_t ay,
                           int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st) {
     if (planes <= 0 || n_arr <= 0) return cudaSuccess;
@@ -1259,15 +1425,16 @@ static bool make_map(CUtensorMap *m, const float *base, int64_t pitch, int64_t a
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TY>
+template <int TY, int NF>
 static cudaError_t launch_stencil(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay,
                                   int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, StepArgs a,
                                   cudaStream_t st) {
     if (z_hi <= z_lo) return cudaSuccess;
-    const size_t smem = sizeof(S2Smem<TY>);
+    using SM = std::conditional_t<NF == 0, S2Smem<TY>, S2SmemF<TY, NF>>;
+    const size_t smem = sizeof(SM);
     // per device (the attribute is per function and device); idempotent, so racing threads are harmless
-    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(stencil_step_tma_kernel<TY, NF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mP, mPP, mV;
     if (!make_map(&mP, pcurr, pitch, ay, planes, S2T<TY>::PW, S2T<TY>::PH) ||
@@ -1284,12 +1451,16 @@ static cudaError_t launch_stencil(const float *vel, float *pprev, const float *p
     a.dt = dt;
     const int gx = (a.nx + S2_TX - 1) / S2_TX, gy = (a.ny + TY - 1) / TY;
     a.gx = gx;
-    // split z so the grid is close to a whole number of waves
+    // split z so the grid is close to a whole number of waves (the fused decode: whole 4-plane slabs)
     const int Z = (int)(z_hi - z_lo), tiles = gx * gy, res = 148 * S2T<TY>::CTAS;
+    auto chunk_of = [&](int nzc) {
+        const int c = (Z + nzc - 1) / nzc;
+        return NF ? (c + 3) & ~3 : c;
+    };
     int best = 1;
     double best_eff = 0;
     for (int nzc = 1; nzc <= 16; ++nzc) {
-        const int chunk = (Z + nzc - 1) / nzc;
+        const int chunk = chunk_of(nzc);
         if (nzc > 1 && chunk < 24) break;
         const int items = tiles * ((Z + chunk - 1) / chunk);
         const double waves = (double)items / res;
@@ -1299,10 +1470,10 @@ static cudaError_t launch_stencil(const float *vel, float *pprev, const float *p
             best = nzc;
         }
     }
-    a.zchunk = (Z + best - 1) / best;
+    a.zchunk = chunk_of(best);
     const int nzc = (Z + a.zchunk - 1) / a.zchunk;
     dim3 grid(gx, gy, nzc);
-    stencil_step_tma_kernel<TY><<<grid, S2T<TY>::THREADS, smem, st>>>(mP, mPP, mV, a);
+    stencil_step_tma_kernel<TY, NF><<<grid, S2T<TY>::THREADS, smem, st>>>(mP, mPP, mV, a);
     return cudaGetLastError();
 }
 
@@ -1352,7 +1523,23 @@ cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int6
         return cudaGetLastError();
     }
     StepArgs a{};
-    return launch_stencil<16>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+    return launch_stencil<16, 0>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
+}
+
+bool step_fused_ok(int q) { return q <= 15 && (q & 1); }
+
+cudaError_t launch_step_fused(const float *vel, float *pprev, const float *pcurr, const void *rec_pprev, int64_t ax,
+                              int64_t ay, int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
+                              cudaStream_t st) {
+    // whole slabs of 16-byte aligned records
+    if (!step_fused_ok(q) || (z_lo & 3) || (reinterpret_cast<uintptr_t>(rec_pprev) & 15)) return cudaErrorInvalidValue;
+    StepArgs a{};
+    a.rec[0] = static_cast<const uint32_t *>(rec_pprev);
+    a.nbx = (int)(ax / 4);
+    a.nby = (int)(ay / 4);
+    a.q = q;
+    a.recw = 2 * (q + 1);
+    return launch_stencil<16, 1>(vel, pprev, pcurr, ax, ay, pitch, planes, z_lo, z_hi, dt, a, st);
 }
 
 // max |x| over rows of n floats (CFL check of a loaded velocity); float bits of non-negative values order

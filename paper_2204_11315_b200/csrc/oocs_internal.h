@@ -52,6 +52,15 @@ cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, 
                           int64_t planes, int64_t pitch, int codec, int q, cudaStream_t st);
 cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, int64_t ax, int64_t ay,
                           int64_t planes, int64_t pitch, int codec, int q, int *err, cudaStream_t st);
+// BlockQuant: decode only the x/y ring blocks of every slab (the rest of the array is the fused step's)
+cudaError_t launch_decode_ring(const void *src, float *dst, int64_t ax, int64_t ay, int64_t planes, int64_t pitch, int q,
+                               cudaStream_t st);
+// the decode -> first step fusion (OOCS_FLAG_FUSE_DECODE): p_prev read from its BlockQuant records
+// (rec_pprev = the records of the working buffer's plane 0, 16-byte aligned; z_lo a multiple of 4)
+bool step_fused_ok(int q);
+cudaError_t launch_step_fused(const float *vel, float *pprev, const float *pcurr, const void *rec_pprev, int64_t ax,
+                              int64_t ay, int64_t pitch, int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int q,
+                              cudaStream_t st);
 cudaError_t launch_step(const float *vel, float *pprev, const float *pcurr, int64_t ax, int64_t ay, int64_t pitch,
                         int64_t planes, int64_t z_lo, int64_t z_hi, float dt, int stencil, cudaStream_t st);
 // max |x| over `rows` rows of `n` floats (row stride `pitch` floats) folded into *out (float bits as u32,

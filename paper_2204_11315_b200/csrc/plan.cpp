@@ -52,12 +52,18 @@ static bool validate(const oocs_config *c, std::string *err) {
         return bad(err, "the uncompressed BASELINE (fig:3ver(a)) is a single-GPU comparison: world must be 1");
     if (c->device < 0) return bad(err, "bad device ordinal");
     if (c->flags & ~(uint32_t)(OOCS_FLAG_PROFILE | OOCS_FLAG_RESIDENT_VELOCITY | OOCS_FLAG_TIMELINE |
-                               OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS | OOCS_FLAG_DECODED_VELOCITY))
+                               OOCS_FLAG_LANE_SINGLE_STREAM | OOCS_FLAG_LANE_SPLIT_STREAMS | OOCS_FLAG_DECODED_VELOCITY |
+                               OOCS_FLAG_FUSE_DECODE))
         return bad(err, "unknown or retired flag (4 = ABI 1's fused last step + encode, removed)");
     if ((c->flags & OOCS_FLAG_RESIDENT_VELOCITY) && (c->store != OOCS_STORE_HOST || c->mode == OOCS_MODE_BASELINE))
         return bad(err, "OOCS_FLAG_RESIDENT_VELOCITY applies to host-store codec modes only");
     if ((c->flags & OOCS_FLAG_DECODED_VELOCITY) && c->store != OOCS_STORE_DEVICE)
         return bad(err, "OOCS_FLAG_DECODED_VELOCITY applies to the device store only");
+    if ((c->flags & OOCS_FLAG_FUSE_DECODE) &&
+        (c->mode == OOCS_MODE_BASELINE || c->codec != OOCS_CODEC_BLOCKQUANT || c->rate_bits > 16 || (c->rate_bits & 1) ||
+         c->stencil != OOCS_STENCIL_ACOUSTIC25))
+        return bad(err, "OOCS_FLAG_FUSE_DECODE applies to codec modes with BlockQuant at an even rate <= 16 and the "
+                        "25-point stencil");
     if (c->schedule < OOCS_SCHED_ALG1 || c->schedule > OOCS_SCHED_DAG_FUNC) return bad(err, "unknown schedule kind");
     if (c->n_lanes != 0 && (c->n_lanes < 2 || c->n_lanes > MAX_LANES)) return bad(err, "n_lanes must be 0 (=3) or 2..8");
     return true;

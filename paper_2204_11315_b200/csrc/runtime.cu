@@ -321,6 +321,41 @@ static oocs_status k_step(Plan *p, const float *v, float *pp, const float *pc, i
     return OOCS_OK;
 }
 
+// decode only the x/y ring of one BlockQuant array (OOCS_FLAG_FUSE_DECODE)
+static oocs_status k_decode_ring(Plan *p, const void *src, float *dst, int64_t planes, cudaStream_t st,
+                                 oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 0);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_decode_ring(src, dst, p->geo.ax, p->geo.ay, planes, p->geo.pitch, p->geo.q, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[0]++;
+        // the ring launch decodes 8 block rows of every line at each y edge and one line (8 blocks) of every
+        // block row at each x edge: about 16 (nbx + nby) blocks per slab
+        const uint64_t blocks = (uint64_t)(planes / 4) * 16 * (uint64_t)(p->geo.ax / 4 + p->geo.ay / 4);
+        stats->alg_bytes[0] += blocks * (64 * 4 + 4 * pb(p) / ((uint64_t)(p->geo.ax / 4) * (p->geo.ay / 4)));
+    }
+    return OOCS_OK;
+}
+
+// the first step of a chunk with p_prev read from its compressed records (OOCS_FLAG_FUSE_DECODE)
+static oocs_status k_step_fused(Plan *p, const float *v, float *pp, const float *pc, const void *rec_pp, int64_t zlo,
+                                int64_t zhi, cudaStream_t st, oocs_stats *stats) {
+    KernelTiming *t = timing_slot(p, 1);
+    if (t) CU(cudaEventRecord(t->a, st));
+    CU(launch_step_fused(v, pp, pc, rec_pp, p->geo.ax, p->geo.ay, p->geo.pitch, p->geo.max_ext, zlo, zhi,
+                         p->geo.cfg.dt, p->geo.q, st));
+    if (t) CU(cudaEventRecord(t->b, st));
+    if (stats) {
+        stats->kernel_launches[1]++;
+        const uint64_t cells = (uint64_t)(zhi - zlo) * p->geo.nx * p->geo.ny;
+        stats->cell_updates_computed += cells;
+        // read p_curr, v and p_prev's records (rate/8 B per value); write p_next
+        stats->alg_bytes[1] += cells * 12 + cells * (uint64_t)p->geo.cfg.rate_bits / 8;
+    }
+    return OOCS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // plan create / destroy
 // ---------------------------------------------------------------------------
@@ -610,6 +645,20 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
 // STEP s updates array (s odd ? 1 : 2) from the other one (leapfrog in place).
 static inline int upd_array(int s) { return (s & 1) ? 1 : 2; }
 
+// compressed source of interior plane z of array a for chunk b (staging slot s, or the device store's S_t)
+static inline const void *comp_src(Plan *p, int s, const oocs_block &b, int a, int64_t z) {
+    const Geometry &g = p->geo;
+    if (a == 0 && p->resident_vel) return p->dvel + hoff(p, z);
+    if (g.host_store) return p->hf[s] + ((uint64_t)a * g.max_ext + (z - b.ext_lo)) * pb(p);
+    return p->dstore[p->cur][a] + hoff(p, z);
+}
+
+// OOCS_FLAG_FUSE_DECODE applies to this chunk: no multi-GPU ghost planes (their p_{t-1} comes from a ghost
+// slot in a second decode), and p_{t-1}'s records of the extent 16-byte aligned
+static inline bool fused_first_step(Plan *p, const oocs_block &b) {
+    return (p->geo.cfg.flags & OOCS_FLAG_FUSE_DECODE) && !ghost_lo(p, b) && !ghost_hi(p, b) && step_fused_ok(p->geo.q);
+}
+
 // Issue one work op (H2D, CARRY, DECODE, STEP, ENCODE, D2H, SEND) on stream st.  The device
 // store's read/write buffers follow from the op's sweep: S_t = dstore[cur0 ^ (sweep & 1)].
 static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cur0, oocs_stats *stats) {
@@ -683,15 +732,32 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         break;
     }
     case OOCS_OP_DECODE: {
-        // compressed source of interior plane z of array a for this chunk
-        auto src_of = [&](int a, int64_t z) -> const void * {
-            if (a == 0 && p->resident_vel) return p->dvel + hoff(p, z);
-            if (g.host_store) return p->hf[s] + ((uint64_t)a * g.max_ext + (z - b.ext_lo)) * PB;
-            return p->dstore[p->cur][a] + hoff(p, z);
-        };
+        auto src_of = [&](int a, int64_t z) { return comp_src(p, s, b, a, z); };
         // with the velocity kept decoded only the two pressures are decoded
         const int a0 = p->vdec ? 1 : 0;
         const bool glo = ghost_lo(p, b), ghi = ghost_hi(p, b);
+        if (fused_first_step(p, b)) {
+            // the velocity and p_t in one launch; of p_{t-1} only what the later steps read beyond the fused
+            // first step's output: the x/y ring, and the physical z-halo planes of a boundary chunk
+            const void *src[2];
+            float *dst[2];
+            int n = 0;
+            if (!a0) {
+                src[n] = src_of(0, b.ext_lo);
+                dst[n++] = wsa(p, w, 0);
+            }
+            src[n] = src_of(2, b.ext_lo);
+            dst[n++] = wsa(p, w, 2);
+            if (oocs_status r = k_decode(p, src, dst, n, E, st, stats)) return r;
+            if (oocs_status r = k_decode_ring(p, src_of(1, b.ext_lo), wsa(p, w, 1), E, st, stats)) return r;
+            if (b.ext_lo == -R)
+                if (oocs_status r = k_decode(p, src_of(1, b.ext_lo), wsa(p, w, 1), R, st, stats)) return r;
+            if (b.ext_hi == g.nz + R)
+                if (oocs_status r = k_decode(p, src_of(1, b.ext_hi - R), wsa(p, w, 1) + (E - R) * g.pstride, R, st,
+                                             stats))
+                    return r;
+            break;
+        }
         if (!glo && !ghi) {
             const void *src[N_ARRAYS];
             float *dst[N_ARRAYS];
@@ -740,8 +806,11 @@ static oocs_status issue_work(Plan *p, const oocs_op &o, cudaStream_t st, int cu
         const int64_t lo = (b.ext_lo == -R) ? 0 : b.ext_lo + (int64_t)sidx * R;
         const int64_t hi = (b.ext_hi == g.nz + R) ? g.nz : b.ext_hi - (int64_t)sidx * R;
         const int up = upd_array(sidx), other = 3 - up;
-        oocs_status r = k_step(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo, hi - b.ext_lo,
-                               st, stats);
+        oocs_status r = sidx == 1 && fused_first_step(p, b)
+                            ? k_step_fused(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other),
+                                           comp_src(p, s, b, up, b.ext_lo), lo - b.ext_lo, hi - b.ext_lo, st, stats)
+                            : k_step(p, vel_of(p, w, b), wsa(p, w, up), wsa(p, w, other), lo - b.ext_lo,
+                                     hi - b.ext_lo, st, stats);
         if (r) return r;
         break;
     }

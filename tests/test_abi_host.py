@@ -46,11 +46,19 @@ def cfg(**kw):
     dict(stencil=2), dict(v_max=-1.0), dict(v_max=float("nan")),
     dict(dt=0.1, v_max=4.53),            # 0.453 > 2/sqrt(3*2048/315) = 0.45286 (ACOUSTIC25 CFL, Q1)
     dict(dt=0.1, v_max=5.78, stencil="star7"),  # 0.578 > 2/sqrt(12) = 0.57735
+    # the decode -> first step fusion: BlockQuant at an even rate <= 16, codec modes, the 25-point stencil
+    dict(fuse_decode=True, rate_bits=24), dict(fuse_decode=True, rate_bits=15), dict(fuse_decode=True, codec="zfp"),
+    dict(fuse_decode=True, mode="baseline", codec="identity"), dict(fuse_decode=True, stencil="star7"),
 ])
 def test_config_errors(kw):
     with pytest.raises(oocs.OocsError) as e:
         oocs.oocs_plan_table(cfg(**kw))
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("rate", [8, 12, 16])
+def test_fuse_decode_accepted(rate):
+    oocs.oocs_plan_table(cfg(fuse_decode=True, rate_bits=rate))
 
 
 @pytest.mark.parametrize("stencil,vdt", [("acoustic25", 0.4528), ("star7", 0.4529), ("star7", 0.5773)])

@@ -13,8 +13,10 @@ nx, ny, nz, nb, k, T, rate = bench.WORKLOADS[os.environ.get("WL", "c2")]
 codec = sys.argv[sys.argv.index("--codec") + 1] if "--codec" in sys.argv else "blockquant"
 if codec == "trunc16":
     rate = 16
+# FUSE=1: the decode -> first step fusion (per interior chunk: decode of v and p_t, ring decode of p_{t-1},
+# the fused first step, 3 steps, encode)
 c = oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, rate_bits=rate,
-                     mode="swb", store="device", codec=codec)
+                     mode="swb", store="device", codec=codec, fuse_decode=os.environ.get("FUSE") == "1")
 pl = oocs.Plan(c)
 bench.load_state(pl, nx, ny, nz, 0)
 pl.run(k)
