@@ -113,9 +113,9 @@ struct LineTask {
 // ring_nl > 0 (decode only): a compact grid over the x/y ring of the allocated grid -- x in [0, 2 nl):
 // the first / last group of 8 block rows of every line, x in [2 nl, 2 nl + 2 ng): the first / last line of
 // every group (corners twice, same values)
-__device__ __forceinline__ LineTask line_task(int nbx, int bz, int ring_nl = 0, int ring_ng = 0) {
+__device__ __forceinline__ LineTask line_task(int nbx, int bz, int grp, int ring_nl = 0, int ring_ng = 0) {
     LineTask t;
-    int L = blockIdx.x, grp = blockIdx.y;
+    int L = blockIdx.x;
     if (ring_nl) {
         int i = blockIdx.x;
         if (i < 2 * ring_nl) {
@@ -137,13 +137,15 @@ __device__ __forceinline__ LineTask line_task(int nbx, int bz, int ring_nl = 0, 
 
 constexpr int CODEC_WARPS = 8;
 
-// up to 3 arrays of one chunk in one launch (grid z = array * slabs + slab): one ramp and one tail
+// up to 3 arrays of one chunk in one launch (grid y = array * gy + row group, z = slab): one ramp and one tail
 // per chunk instead of one per array
 struct CodecArrays {
     const void *src[N_ARRAYS];
     void *dst[N_ARRAYS];
-    int slabs;  // 4-plane slabs per array
+    int gy;                // grid y per array (groups of 8 block rows; 1 for the ring grid): y = array * gy + group
     int ring_nl, ring_ng;  // decode: > 0 = the x/y ring only (line_task)
+    // array and row group of this CTA from blockIdx.y (<= 3 arrays: two compares, no integer division)
+    __device__ __forceinline__ int array() const { return (blockIdx.y >= (unsigned)gy) + (blockIdx.y >= 2u * gy); }
     // selects, not a dynamic index: an indexed kernel-parameter array would be copied to local memory
     __device__ __forceinline__ const void *in(int a) const { return a == 0 ? src[0] : a == 1 ? src[1] : src[2]; }
     __device__ __forceinline__ void *out(int a) const { return a == 0 ? dst[0] : a == 1 ? dst[1] : dst[2]; }
@@ -161,10 +163,10 @@ bq_decode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
     const int q = QT ? QT : q_rt;
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int arr = blockIdx.z / A.slabs;
+    const int arr = A.array();
     const uint8_t *__restrict__ src = static_cast<const uint8_t *>(A.in(arr));
     float *__restrict__ dst = static_cast<float *>(A.out(arr));
-    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs, A.ring_nl, A.ring_ng);
+    const LineTask t = line_task(nbx, blockIdx.z, blockIdx.y - arr * A.gy, A.ring_nl, A.ring_ng);
     if (t.by >= nby) return;
     const int recw = 2 * (q + 1);  // record size in 32-bit words
     const uint32_t *rec0 = reinterpret_cast<const uint32_t *>(src) +
@@ -345,23 +347,24 @@ bq_encode_kernel(const CodecArrays A, int nbx, int nby, int64_t pitch, int64_t p
     const int q = QT ? QT : q_rt;
     __shared__ __align__(16) uint32_t codes[CODEC_WARPS][8][CODE_LD];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int arr = blockIdx.z / A.slabs;
+    const int arr = A.array();
     const float *__restrict__ src = static_cast<const float *>(A.in(arr));
     uint8_t *__restrict__ dst = static_cast<uint8_t *>(A.out(arr));
-    const LineTask t = line_task(nbx, blockIdx.z - arr * A.slabs);
+    const LineTask t = line_task(nbx, blockIdx.z, blockIdx.y - arr * A.gy);
     if (t.by >= nby) return;
     // ---- load straight into the statistics layout: lane -> block ib, rows r0, r0+4, r0+8, r0+12
-    //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging)
+    //      (per instruction 4 rows x 128 contiguous bytes: coalesced, no shared-memory staging).  Row
+    //      r = yi + 4 zi = r0 + 4u is plane u, row r0 of the slab.  Lanes of blocks past the line's end
+    //      (ib >= nb, first and last line only) read the rest of their 128-byte line -- inside the row's
+    //      pitch -- and are never stored, so every load is unconditional
     const int ib = lane & 7, r0 = lane >> 3;
     const bool live = ib < t.nb;
-    const float *sbase = src + (int64_t)(4 * t.bz) * pstride + (int64_t)(4 * t.by) * pitch + XOFF + 4 * t.b0 + 4 * ib;
+    const float4 *sbase = reinterpret_cast<const float4 *>(src + (int64_t)(4 * t.bz) * pstride +
+                                                           (int64_t)(4 * t.by + r0) * pitch + XOFF + 4 * t.b0 + 4 * ib);
+    const int64_t ps4 = pstride / 4;  // pitch (hence pstride) is a multiple of 32 floats
     float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 4 * u;  // r = yi + 4 zi
-        v[u] = live ? __ldcs(reinterpret_cast<const float4 *>(sbase + (int64_t)(r >> 2) * pstride + (int64_t)(r & 3) * pitch))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(sbase + u * ps4);
     const int recw = 2 * (q + 1);
     uint32_t *rec0 = reinterpret_cast<uint32_t *>(dst) + ((int64_t)(t.bz * nby + t.by) * nbx + t.b0) * recw;
     const bool bad = bq_encode_core<TWO, QT>(v, live, (1u << t.nb) - 1u, rec0, q, codes[warp], lane);
@@ -1233,8 +1236,8 @@ cudaError_t launch_decode(const void *const *src, float *const *dst, int n_arr, 
             A.src[a] = src[a];
             A.dst[a] = dst[a];
         }
-        A.slabs = (int)(planes / 4);
-        const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(A.slabs * n_arr));
+        A.gy = (nby + 7) / 8;
+        const dim3 blocks((unsigned)nl, (unsigned)(A.gy * n_arr), (unsigned)(planes / 4));
 #define DEC(TWO, QT) bq_decode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q)
         switch (q) {  // the BASELINE.json rate sweep 8/12/16/24 bits/value gets constant-folded kernels
         case 7: DEC(false, 7); break;
@@ -1283,10 +1286,10 @@ cudaError_t launch_decode_ring(const void *src, float *dst, int64_t ax, int64_t 
     CodecArrays A{};
     A.src[0] = src;
     A.dst[0] = dst;
-    A.slabs = (int)(planes / 4);
+    A.gy = 1;
     A.ring_nl = (int)nlines_of(ax);
     A.ring_ng = (nby + 7) / 8;
-    const dim3 blocks((unsigned)(2 * A.ring_nl + 2 * A.ring_ng), 1u, (unsigned)A.slabs);
+    const dim3 blocks((unsigned)(2 * A.ring_nl + 2 * A.ring_ng), 1u, (unsigned)(planes / 4));
     const int64_t pstride = ay * pitch;
 #define DEC(TWO, QT) bq_decode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q)
     switch (q) {
@@ -1314,8 +1317,8 @@ cudaError_t launch_encode(const float *const *src, void *const *dst, int n_arr, 
             A.src[a] = src[a];
             A.dst[a] = dst[a];
         }
-        A.slabs = (int)(planes / 4);
-        const dim3 blocks((unsigned)nl, (unsigned)((nby + 7) / 8), (unsigned)(A.slabs * n_arr));
+        A.gy = (nby + 7) / 8;
+        const dim3 blocks((unsigned)nl, (unsigned)(A.gy * n_arr), (unsigned)(planes / 4));
 #define ENC(TWO, QT) bq_encode_kernel<TWO, QT><<<blocks, CODEC_WARPS * 32, 0, st>>>(A, nbx, nby, pitch, pstride, q, err)
         switch (q) {
         case 7: ENC(false, 7); break;
