@@ -30,8 +30,12 @@ def entry(rep, alg, unit, idx=0):
 
 
 def codec_values(rep, idx=0):
-    gz = int(summarise(rep)[idx]["grid"].strip("()").split(",")[2])
-    return 4 * gz * AX * AX, 4 * gz
+    # grid (lines, arrays x row groups, slabs) since the codec kernels take the array from grid y (round 2;
+    # before: grid z = arrays x slabs, grid y = row groups)
+    _, gy, gz = (int(x) for x in summarise(rep)[idx]["grid"].strip("()").split(","))
+    groups = (AX // 4 + 7) // 8
+    planes = 4 * gz * (gy // groups)
+    return planes * AX * AX, planes
 
 
 if __name__ == "__main__":
