@@ -91,3 +91,13 @@ def test_fused_split_runs_equal_one_run():
     ref, _ = run(nx, ny, nz, n, k, 8, False)
     got, _ = run(nx, ny, nz, n, k, 8, True, split=[2, 4, 2])
     assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
+
+
+@pytest.mark.parametrize("store", ["host", "device"])
+def test_fused_medium_grid_z_split(store):
+    # 512^2 planes: 256 tiles < 296 resident CTAs, so the step's z range is split across CTAs (the fused
+    # kernel rounds each CTA's z range to whole 4-plane slabs); 4 chunks, k = 4, two sweeps
+    nx, ny, nz, n, k = 512, 512, 256, 4, 4
+    ref, _ = run(nx, ny, nz, n, k, 8, False, store=store)
+    got, _ = run(nx, ny, nz, n, k, 8, True, store=store)
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
