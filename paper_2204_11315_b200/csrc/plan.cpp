@@ -375,6 +375,9 @@ static void footprint(const Geometry &geo, const oocs_op &o, std::vector<Acc> &f
         f.push_back({2, w, 0, lo - R - b.ext_lo, hi + R - b.ext_lo, false});
         f.push_back({2, w, 3 - up, lo - R - b.ext_lo, hi + R - b.ext_lo, false});
         f.push_back({2, w, up, lo - b.ext_lo, hi - b.ext_lo, true});
+        // OOCS_FLAG_FUSE_DECODE: the first step reads p_{t-1}'s records in the staging buffer (edge chunks of
+        // a multi-GPU run are not fused; the extra edge is then only conservative)
+        if (o.arg == 1 && (geo.cfg.flags & OOCS_FLAG_FUSE_DECODE) && !base) f.push_back({1, s, -1, ME, ME + E, false});
         break;
     }
     case OOCS_OP_ENCODE:

@@ -78,6 +78,10 @@ def footprint(op, blocks, geo):
         for a in (0, 3 - up):
             out.append((("ws", w, a), lo - R - ext_lo, hi + R - ext_lo, False))
         out.append((("ws", w, up), lo - ext_lo, hi - ext_lo, True))
+        if st == 1 and geo.get("fuse_decode"):
+            # OOCS_FLAG_FUSE_DECODE: the first step reads p_{t-1} from its compressed records in the staging
+            # buffer (the decode then writes only p_{t-1}'s ring, still modelled as the whole array)
+            out.append((("hf", s), ME, ME + E, False))
     elif kind == "ENCODE":
         for a in (1, 2):
             out.append((("ws", w, a), own_lo - ext_lo, own_hi - ext_lo, False))

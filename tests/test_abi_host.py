@@ -107,7 +107,8 @@ def _geo(c, blocks):
     n_ws = {0: L, 1: L, 2: 1, 3: 2}[c.mode] if c.store == 0 else 1
     return dict(k=c.tb_depth, n_ws=n_ws, lanes=L, mode={0: "baseline"}.get(c.mode, "codec"), nz=c.nz,
                 max_ext=max(b[3] - b[2] for b in blocks), max_own=max(b[1] - b[0] for b in blocks),
-                resident_velocity=bool(c.flags & oocs.FLAG_RESIDENT_VELOCITY))
+                resident_velocity=bool(c.flags & oocs.FLAG_RESIDENT_VELOCITY),
+                fuse_decode=bool(c.flags & oocs.FLAG_FUSE_DECODE))
 
 
 def _check(c, steps):
@@ -131,6 +132,32 @@ def test_schedule_is_race_free(mode, codec, n, k, nz, lanes, sched):
     assert bad == [], bad[:5]
     # every chunk of every sweep is decoded/computed/encoded exactly once per step
     assert sum(o["kind"] == "STEP" for o in ops) == 3 * n * k
+
+
+@pytest.mark.parametrize("sched", ["alg1", "dag", "dag_func"])
+@pytest.mark.parametrize("lanes", [0, 2, 4])
+@pytest.mark.parametrize("mode", ["swb", "dwb", "compress"])
+@pytest.mark.parametrize("resident", [False, True])
+@pytest.mark.parametrize("n,k,nz", [(1, 1, 16), (3, 2, 48), (5, 3, 80), (12, 1, 96)])
+def test_schedule_is_race_free_with_fused_first_step(mode, n, k, nz, lanes, sched, resident):
+    # OOCS_FLAG_FUSE_DECODE adds a read of the staging buffer (p_{t-1}'s records) to every chunk's first step
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, n_lanes=lanes, schedule=sched, fuse_decode=True,
+            resident_velocity=resident)
+    ops, bad = _check(c, 3 * k)
+    assert bad == [], bad[:5]
+
+
+def test_fused_first_step_read_is_guarded():
+    # the model sees the fused read: deleting the waits that order the next H2D into a staging slot after
+    # that slot's chunk is done (its D2H) exposes the first step's read, not only the decode's
+    c = cfg(nz=64, n_blocks=4, tb_depth=2, mode="swb", fuse_decode=True)
+    ops = oocs.oocs_schedule(c, 4)
+    blocks = oocs.oocs_plan_table(c)
+    geo = _geo(c, blocks)
+    assert sc.violations(ops, blocks, geo) == []
+    fused_reads = [i for i, o in enumerate(ops) if o["kind"] == "STEP" and o["arg"] == 1]
+    assert fused_reads and any(r[0] == ("hf", ops[fused_reads[0]]["g"] % 3)
+                               for r in sc.footprint(ops[fused_reads[0]], blocks, geo))
 
 
 def test_algorithm1_golden_n3():
@@ -384,14 +411,15 @@ def test_schedule_race_free_random_configs():
         done += 1
 
 
+@pytest.mark.parametrize("fuse", [False, True])
 @pytest.mark.parametrize("mode", ["swb", "dwb", "compress"])
 @pytest.mark.parametrize("n,k,nz,lanes", [(4, 2, 64, 0), (16, 1, 128, 2), (2, 1, 32, 0), (5, 3, 80, 2), (1, 1, 16, 0)])
-def test_chained_runs_are_race_free(mode, n, k, nz, lanes):
+def test_chained_runs_are_race_free(mode, n, k, nz, lanes, fuse):
     """oocs_run_async issues a run while the previous one drains: the dispatcher sees the two op lists
     back to back (lane programs and events continue across them).  Their concatenation must be race-free
     under stream + event semantics, and the second run's first H2Ds must carry the cross-sweep waits on
     the first run's write-backs -- deleting them is a detected race."""
-    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, n_lanes=lanes)
+    c = cfg(nz=nz, n_blocks=n, tb_depth=k, mode=mode, n_lanes=lanes, fuse_decode=fuse)
     s1, s2, s3 = 2 * k, k, 3 * k
     ops = (oocs.oocs_schedule(c, s1) + oocs.oocs_schedule(c, s2, first_sweep=s1 // k)
            + oocs.oocs_schedule(c, s3, first_sweep=(s1 + s2) // k))

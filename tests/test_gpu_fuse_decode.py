@@ -78,6 +78,11 @@ def test_fused_first_step_bitwise(nx, ny, nz, n, k, rate):
     ("swb", "host", {"n_lanes": 2}),
     ("swb", "host", {"schedule": "dag"}),
     ("swb", "host", {"schedule": "dag_func", "executor": "split"}),
+    # the DAG schedules must order the next H2D into a staging slot after the fused step's read of it (the
+    # race checker found this edge missing with the resident velocity, where the encode output no longer
+    # overlaps p_{t-1}'s input region)
+    ("swb", "host", {"schedule": "dag_func", "resident_velocity": True, "n_lanes": 2}),
+    ("dwb", "host", {"schedule": "dag", "resident_velocity": True}),
 ])
 def test_fused_modes_bitwise(mode, store, kw):
     nx, ny, nz, n, k = 136, 52, 128, 4, 2
