@@ -32,9 +32,12 @@ def _cuda():
 
 def _cfg(codec, store, mode, rank=0, world=1, nb=NB, k=K, rate=16):
     dec = store == "device_decv"  # device store with the velocity kept decoded (OOCS_FLAG_DECODED_VELOCITY)
+    fuse = store.endswith("_fuse")  # OOCS_FLAG_FUSE_DECODE: interior chunks fused, edge chunks (ghost planes) not
+    store = store[:-5] if fuse else store
     return oocs.make_config(nx=NX, ny=NY, nz=NZ, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k, codec=codec,
                             rate_bits=rate if codec != "identity" else 32, mode=mode,
-                            store="device" if dec else store, rank=rank, world=world, decoded_velocity=dec)
+                            store="device" if dec else store, rank=rank, world=world, decoded_velocity=dec,
+                            fuse_decode=fuse)
 
 
 def _load(pl):
@@ -117,7 +120,8 @@ def _single(args, T):
 
 
 CASES = [("blockquant", "host", "swb"), ("blockquant", "device", "swb"), ("identity", "host", "dwb"),
-         ("blockquant", "device_decv", "swb"), ("zfp", "host", "compress"), ("trunc16", "host", "swb")]
+         ("blockquant", "device_decv", "swb"), ("zfp", "host", "compress"), ("trunc16", "host", "swb"),
+         ("blockquant", "host_fuse", "swb"), ("blockquant", "device_fuse", "swb")]
 
 
 @pytest.mark.parametrize("args", CASES, ids=lambda a: "-".join(a))
