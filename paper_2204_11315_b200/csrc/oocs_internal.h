@@ -32,7 +32,9 @@ struct Geometry {
     int64_t store_lo, store_hi;      // interior planes held by this rank's store (owned + ghost)
     int64_t max_ext, max_own;        // planes
     int n_ws;               // working sets
-    int lanes;              // CUDA streams = half-size buffers
+    int lanes;              // half-size buffers (chunk g uses slot g mod lanes) = CUDA streams of Alg. 1
+    int nstreams;           // op lanes of the schedule: lanes, or 3 for OOCS_SCHED_DAG_FUNC (H2D+carry / kernels
+                            // / D2H) when lanes < 3
     bool host_store;
     int64_t a_store_lo() const { return store_lo + R; }  // allocated plane of store index 0
     int64_t store_planes() const { return store_hi - store_lo; }

@@ -131,6 +131,9 @@ oocs_status make_geometry(const oocs_config *cfg, Geometry *g, std::string *err)
     }
     g->host_store = c.store == OOCS_STORE_HOST;
     g->lanes = c.n_lanes ? c.n_lanes : 3;
+    // the by-function DAG schedule runs its ops on three streams (H2D + carry / kernels / D2H) whatever the
+    // number of staging slots
+    g->nstreams = (g->host_store && c.schedule == OOCS_SCHED_DAG_FUNC) ? std::max(g->lanes, 3) : g->lanes;
     if (!g->host_store)
         g->n_ws = 1;
     else  // SWB: one working buffer; DWB: two; BASELINE / COMPRESS: one per stream (fig:3ver)

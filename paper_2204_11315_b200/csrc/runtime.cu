@@ -590,7 +590,7 @@ static oocs_status create(const oocs_config *cfg, Plan **out, void *ext_arena = 
         const char *env = std::getenv("OOCS_COPY_CHUNK_MB");
         p->copy_chunk = env ? (uint64_t)(std::strtod(env, nullptr) * 1048576.0) & ~uint64_t(15) : 0;
     }
-    for (int l = 0; l < g.lanes; ++l) {
+    for (int l = 0; l < g.nstreams; ++l) {
         // a caller stream (oocs_config.ext_streams) is the lane's kernel stream (its only stream with
         // LANE_SINGLE_STREAM); it must belong to the plan's device
         cudaStream_t ext = static_cast<cudaStream_t>(g.cfg.ext_streams[l]);
@@ -927,7 +927,7 @@ static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int
     };
     std::vector<cudaStream_t> op_stream(ops.size());
     {
-        std::vector<cudaStream_t> next(g.lanes, nullptr), prev(g.lanes, nullptr);
+        std::vector<cudaStream_t> next(g.nstreams, nullptr), prev(g.nstreams, nullptr);
         for (size_t i = ops.size(); i-- > 0;) {
             const oocs_op &o = ops[i];
             if (is_work_op(o.kind)) next[o.lane] = work_stream(o);
@@ -939,7 +939,7 @@ static oocs_status execute_streams(Plan *p, const std::vector<oocs_op> &ops, int
             else if (o.kind == OOCS_OP_RECORD) op_stream[i] = prev[o.lane] ? prev[o.lane] : p->lanes[o.lane];
         }
     }
-    std::vector<cudaStream_t> last_work(g.lanes, nullptr);
+    std::vector<cudaStream_t> last_work(g.nstreams, nullptr);
     for (size_t oi = 0; oi < ops.size(); ++oi) {
         const oocs_op &o = ops[oi];
         cudaStream_t st = op_stream[oi];
@@ -1008,9 +1008,9 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
     // events live in the other slot's op_done pool
     std::vector<int64_t> dep_start(n + 1, 0), deps, fdep_start(n + 1, 0), fdeps;
     {
-        std::vector<int64_t> last_work(g.lanes, -1);
+        std::vector<int64_t> last_work(g.nstreams, -1);
         for (auto &m : me.producer) m.clear();
-        std::vector<std::vector<int64_t>> lane_waits(g.lanes), lane_fwaits(g.lanes);
+        std::vector<std::vector<int64_t>> lane_waits(g.nstreams), lane_fwaits(g.nstreams);
         for (size_t i = 0; i < n; ++i) {
             const oocs_op &o = ops[i];
             dep_start[i] = (int64_t)deps.size();
@@ -1040,8 +1040,8 @@ static oocs_status execute_dispatch(Plan *p, const std::vector<oocs_op> &ops, in
         fdep_start[n] = (int64_t)fdeps.size();
         // a run of a plan with no chained successor keeps lanes that never worked pointing at the
         // predecessor's last op on them (chains skip none, but keep the state total)
-        me.lane_last.assign(g.lanes, -1);
-        for (int l = 0; l < g.lanes; ++l) me.lane_last[l] = last_work[l];
+        me.lane_last.assign(g.nstreams, -1);
+        for (int l = 0; l < g.nstreams; ++l) me.lane_last[l] = last_work[l];
     }
     std::vector<cudaEvent_t> &done_ev = p->op_done[slot];
     if (done_ev.size() < n) {
@@ -1270,9 +1270,9 @@ static oocs_status submit(Plan *p, int64_t steps, bool chain) {
         // nothing in flight: clear the error flag, and anchor every stream at the run's start mark
         CU(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->tstream));
         CU(cudaEventRecord(p->t0[slot], p->tstream));
-        for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0[slot], 0));
+        for (int l = 0; l < g.nstreams; ++l) CU(cudaStreamWaitEvent(p->lanes[l], p->t0[slot], 0));
         if (p->split)
-            for (int l = 0; l < g.lanes; ++l) CU(cudaStreamWaitEvent(p->klanes[l], p->t0[slot], 0));
+            for (int l = 0; l < g.nstreams; ++l) CU(cudaStreamWaitEvent(p->klanes[l], p->t0[slot], 0));
         for (int c = 0; c < 3; ++c) CU(cudaStreamWaitEvent(p->cstream[c], p->t0[slot], 0));
     } else {
         // the mark follows the previous run's t1 on the timing stream: the time this run's first ops
@@ -1282,7 +1282,7 @@ static oocs_status submit(Plan *p, int64_t steps, bool chain) {
     oocs_status st = execute(p, ops, &r.stats, chained ? &p->runs[prev] : nullptr);
     if (st) return poison(p, st);
     // t1: after every stream's share of this run
-    for (int l = 0; l < g.lanes; ++l) {
+    for (int l = 0; l < g.nstreams; ++l) {
         CU(cudaEventRecord(p->lane_done[l], p->lanes[l]));
         CU(cudaStreamWaitEvent(p->tstream, p->lane_done[l], 0));
         if (p->split) {
