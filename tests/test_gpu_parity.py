@@ -279,6 +279,9 @@ def test_lossy_modes_are_bitwise_identical(rate):
     # instead of the host dispatcher
     variants += [v + (ex,) for ex in ("single", "split") for v in variants[:4] + variants[6:8]]
     variants += [("swb", "host", False, 2, "alg1")]  # the bench's out-of-core configuration (2 lanes)
+    # the by-function DAG schedule runs three streams whatever the lane count (n_lanes = 2 once crashed)
+    variants += [("swb", "host", False, 2, "dag_func"), ("swb", "host", True, 2, "dag_func", "single"),
+                 ("dwb", "host", False, 2, "dag_func", "split")]
     for mode, store, resident, lanes, sched, *ex in variants:
         pl = make_plan(nx, ny, nz, 4, 2, rate=rate, mode=mode, store=store, resident_velocity=resident,
                        n_lanes=lanes, schedule=sched, executor=ex[0] if ex else "dispatch")
