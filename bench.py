@@ -464,7 +464,7 @@ def main():
     dt = float(__import__("synth").dt_for())
 
     def mk(store, mode="swb", codec=None, profile=False, resident_velocity=False, decoded_velocity=False,
-           wl=None):
+           wl=None, fuse=None):
         codec = codec or args.codec
         wnx, wny, wnz, wnb = (nx, ny, nz, nblocks) if wl is None else wl
         c = oocs.make_config(nx=wnx, ny=wny, nz=wnz, dt=dt, n_blocks=wnb, tb_depth=k, codec=codec,
@@ -472,7 +472,8 @@ def main():
                              rank=rank if wl is None else 0, world=world if wl is None else 1,
                              profile=profile, resident_velocity=resident_velocity, schedule=args.schedule,
                              decoded_velocity=decoded_velocity, n_lanes=0 if mode == "baseline" else args.lanes,
-                             fuse_decode=args.fuse_decode and mode != "baseline" and codec == "blockquant")
+                             fuse_decode=(args.fuse_decode if fuse is None else fuse) and mode != "baseline"
+                             and codec == "blockquant")
         pl = oocs.Plan(c)
         if world > 1 and wl is None:
             odist.connect(pl, gloo=gloo)
@@ -635,6 +636,25 @@ def main():
                          "encode_GBps": ad["alg"][2] / (ad["kernel_ms"][2] * 1e-3) / 1e9,
                          "kernel_share_of_step": sum(ad["kernel_ms"]) / ad["ms"]}
             dvp.close()
+            # the same with the decode -> first step fusion (OOCS_FLAG_FUSE_DECODE, NEXT-2): bitwise the same
+            # state, p_{t-1} read from its records inside the first step
+            if args.codec == "blockquant" and rate <= 16 and rate % 2 == 0 and not args.fuse_decode:
+                dvf = mk("device", profile=True, fuse=True)
+                copy_state(host, dvf)
+                for _ in range(min(args.warmup, 3)):
+                    dvf.run(T)
+                barrier()
+                per_f = [dvf.run(T) for _ in range(args.steps)]
+                barrier()
+                af = agg(per_f)
+                f_ms = allmax(af["ms"])
+                vf = allsum(af["cells"]) / (f_ms * 1e-3) / 1e9
+                value_dev["fused_first_step"] = {
+                    "value": vf, "unit": UNIT, "ms_per_step": f_ms / args.steps, "vs_unfused": vf / value_dev["value"],
+                    "kernel_ms": dict(zip(["decode", "step", "encode"], af["kernel_ms"])),
+                    "unfused_kernel_ms": dict(zip(["decode", "step", "encode"], ad["kernel_ms"])),
+                    "flag": "OOCS_FLAG_FUSE_DECODE (opt-in; --fuse-decode runs every plan of the bench with it)"}
+                dvf.close()
         else:
             value_dev = {"value": None, "skipped": f"needs {need / 1e9:.1f} GB of HBM"}
     # ---- variant: the read-only velocity kept compressed in HBM (OOCS_FLAG_RESIDENT_VELOCITY):
