@@ -57,10 +57,10 @@ CASES = [
     (64, 32, 128, 4, 4),
     (200, 72, 64, 2, 3),
     (40, 36, 160, 5, 1),
-    # degenerate: the smallest grid (4^2 planes: one tile, 2 x 2 interior blocks), kR = 12 > the 8-plane
+    # degenerate: the smallest grid (4^2 planes: one tile, 2 x 2 interior blocks), 2kR = 16 > the 12-plane
     # chunk width (extents reach past the neighbour chunk), one chunk spanning the domain
     (4, 4, 16, 2, 1),
-    (8, 8, 32, 4, 3),
+    (8, 8, 48, 4, 2),
     (12, 20, 32, 1, 2),
 ]
 
