@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--ks", default="4,8,12,16")
     ap.add_argument("--rates", default="8,16")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_crossover_c3.json"))
+    ap.add_argument("--fuse-decode", action="store_true", help="every plan with OOCS_FLAG_FUSE_DECODE")
     a = ap.parse_args()
     n, nb = a.n, a.nb
     dt = float(synth.dt_for())
@@ -44,7 +45,8 @@ def main():
         for k in [int(x) for x in a.ks.split(",")]:
             T = a.sweeps * k
             mk = lambda store, **kw: oocs.Plan(oocs.make_config(nx=n, ny=n, nz=n, dt=dt, n_blocks=nb, tb_depth=k,
-                                                                rate_bits=r, mode="swb", store=store, **kw))
+                                                                rate_bits=r, mode="swb", store=store,
+                                                                fuse_decode=a.fuse_decode, **kw))
             t0 = time.time()
             dev = mk("device")
             bench.load_state(dev, n, n, n, 0)
@@ -74,7 +76,8 @@ def main():
             rows.append(row)
             print(json.dumps(row), flush=True)
     json.dump({"config": f"BASELINE.json configs[2] grid ({n}^3, {nb} chunks, W = {n // nb}), k x rate, "
-                         f"{a.sweeps} sweeps per oocs_run, best of 3 runs",
+                         f"{a.sweeps} sweeps per oocs_run, best of 3 runs"
+                         + (", decode -> first step fusion (OOCS_FLAG_FUSE_DECODE)" if a.fuse_decode else ""),
                "rows": rows, "pcie": link}, open(a.out, "w"), indent=1)
 
 
