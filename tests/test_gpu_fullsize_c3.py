@@ -295,3 +295,35 @@ def test_sampled_blocks_second_sweep_zfp():
                 json.dump({"case": "c3 zfp k4 r12", "records_compared": n, "records_bit_identical": exact}, f)
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("store", ["device", "host"])
+def test_fused_first_step_full_size_bitwise(store):
+    """The decode -> first step fusion (OOCS_FLAG_FUSE_DECODE) at the bench's c3 configuration, two sweeps
+    from the same S_0: sampled slabs of S_2 (every chunk seam, the domain's edge slabs, random slabs; both
+    pressures) bitwise equal to the unfused run's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    nx = ny = nz = 2048
+    nb, k, rate = 16, 4, 16
+    rec = 8 * rate
+    nbx = nby = (nx + 2 * R) // 4
+    nbz = (nz + 2 * R) // 4
+    W = nz // nb
+    rng = np.random.default_rng(2204)
+    zs = sorted({1, nbz - 2} | {(i * W) // 4 for i in range(1, nb)} | {(i * W) // 4 + 1 for i in range(1, nb, 3)}
+                | {int(z) for z in rng.integers(1, nbz - 1, 6)})
+    got = {}
+    for fuse in (False, True):
+        plan = oocs.Plan(oocs.make_config(nx=nx, ny=ny, nz=nz, dt=float(synth.dt_for()), n_blocks=nb, tb_depth=k,
+                                          codec="blockquant", rate_bits=rate, mode="swb", store=store, n_lanes=2,
+                                          fuse_decode=fuse))
+        try:
+            bench.load_state(plan, nx, ny, nz, 0)
+            plan.run(2 * k)
+            got[fuse] = {(a, z): plan.read_raw(a, 4 * z, 4 * z + 4) for a in (1, 2) for z in zs}
+        finally:
+            plan.close()
+    for key in got[False]:
+        assert got[False][key].size == nby * nbx * rec
+        assert np.array_equal(got[False][key], got[True][key]), (store, key)
