@@ -126,7 +126,10 @@ typedef enum {
  * their lane's kernel stream with device-side waits, copies only once their dependencies have completed,
  * on one stream per direction -- so no copy stream ever holds a pending cross-stream wait (a copy channel
  * blocked on a wait was measured, OOCS_FLAG_TIMELINE, to be re-examined only when the copy engine's
- * current DMA ends: DESIGN.md §8).  These flags replay the schedule onto streams instead:
+ * current DMA ends: DESIGN.md §8) -- except, on chainable plans, a run's trailing write-backs: once only
+ * D2H copies are left they are issued at once behind device-side waits on the D2H stream, so that the
+ * call returns (and a chained next run's H2Ds start) without the host waiting for the last encodes.
+ * These flags replay the schedule onto streams instead:
  * LANE_SINGLE_STREAM = one CUDA stream per lane, the literal mapping of Alg. 1's three streams;
  * LANE_SPLIT_STREAMS = a copy and a kernel stream per lane, joined by an event at every switch.  All
  * three execute the same dependencies and produce the same bytes. */
